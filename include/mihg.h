@@ -1,0 +1,148 @@
+/*
+ * mihg — B200-native exact Hamming k-NN (multi-index hashing), C ABI.
+ *
+ * This is the drop-in boundary for the reference's hot path, the C++ interface in
+ * /root/reference/proj/include/mih (no C ABI exists there). Every entry point is
+ * extern "C", takes plain pointers and sizes, never throws, and returns a status code:
+ *
+ *   MIHG_OK       0
+ *   MIHG_EINVAL   1  <-> std::invalid_argument in the reference (index.hpp:102-112, :187-188,
+ *                       codes.hpp:152-176, table.hpp:273-277)
+ *   MIHG_EINTERNAL 2
+ *   MIHG_ENOMEM   3  <-> std::bad_alloc (table.hpp:59)
+ *   MIHG_ECUDA    4  CUDA runtime / kernel failure
+ *   MIHG_ENCCL    5  (reserved for the multi-GPU layer; the C++/Python hosts raise it)
+ *
+ * mihg_last_error() returns a thread-local message for the last failing call on this thread.
+ *
+ * Code layout (codes.hpp:26-33, :54-120): n records of ceil(bits/64) little-endian u64 words,
+ * bit i at word i/64 bit i%64, padding bits zero; a code's id is its row index.
+ * Result layout: row-major [nq][k] ids and distances ordered by (distance asc, id asc), the
+ * reference's neighbor_less (scan.hpp:24-26) and tie rule (scan.hpp:42, index.hpp:243).
+ *
+ * Threading: an index is immutable after build; calls on one index are serialised internally
+ * (the device workspace is per index). Different indexes may be used concurrently.
+ */
+#ifndef MIHG_H
+#define MIHG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MIHG_OK 0
+#define MIHG_EINVAL 1
+#define MIHG_EINTERNAL 2
+#define MIHG_ENOMEM 3
+#define MIHG_ECUDA 4
+#define MIHG_ENCCL 5
+
+#define MIHG_ABI_VERSION 1
+
+typedef struct mihg_index mihg_index;
+
+/* mih::SearchTrace (index.hpp:45-51). */
+typedef struct mihg_trace {
+  uint64_t lookups;              /* buckets probed */
+  uint64_t candidates;           /* ids retrieved before duplicate suppression */
+  uint64_t unique_candidates;    /* distinct ids retrieved */
+  uint64_t distance_evaluations; /* always equals unique_candidates */
+  uint32_t final_radius;         /* kNN: completed guarantee radius */
+  uint32_t reserved;
+} mihg_trace;
+
+/* Extended build parameters (mihg_index_build covers the common case). */
+typedef struct mihg_build_params {
+  const uint64_t* codes;      /* n * ceil(bits/64) words (host, or device if codes_on_device) */
+  uint64_t n;
+  uint32_t bits;
+  uint32_t m;                 /* number of substrings / tables */
+  const uint32_t* lengths;    /* NULL: consecutive_partition(bits, m) (codes.hpp:198-211) */
+  const uint32_t* positions;  /* concatenated bit positions of substring 0, 1, ... */
+  int device;                 /* CUDA device ordinal */
+  int codes_on_device;        /* 1: `codes` is a device pointer on `device` */
+  uint32_t id_base;           /* global id of local id 0 (id-range shard); 0 for a whole DB */
+  uint32_t dense_max_bits;    /* 0 = default (24): tables with 2^s <= max(2^this, 2n) are dense */
+  int layout;                 /* 0 auto, 1 force dense offsets, 2 force sparse directory */
+} mihg_build_params;
+
+typedef struct mihg_index_info {
+  uint64_t n;
+  uint32_t bits;
+  uint32_t m;
+  uint32_t id_base;
+  int device;
+  uint64_t device_bytes;      /* codes + all tables */
+} mihg_index_info;
+
+/* mih::TableStats (table.hpp:33-47) plus the GPU layout. */
+typedef struct mihg_table_info {
+  uint32_t s;
+  uint32_t dense;             /* 1: offsets[2^s+1]; 0: blocked-count directory */
+  uint64_t non_empty_buckets;
+  uint64_t max_bucket_size;
+  uint64_t total_entries;
+  uint64_t estimated_bytes;   /* the reference's accounting model, TableStats::estimate_bytes */
+  uint64_t device_bytes;      /* this table's actual HBM footprint */
+  uint64_t escaped_blocks;
+} mihg_table_info;
+
+const char* mihg_last_error(void);
+int mihg_abi_version(void);
+int mihg_device_count(int* count);
+
+/* MihIndex::build(CodeDatabase db, Partition partition) — index.hpp:101-121 (and build_index,
+ * index.hpp:287-289). Host codes; lengths/positions NULL -> consecutive_partition(bits, m). */
+int mihg_index_build(const uint64_t* codes, uint64_t n, uint32_t bits, uint32_t m,
+                     const uint32_t* lengths, const uint32_t* positions, int device,
+                     mihg_index** out);
+int mihg_index_build_ex(const mihg_build_params* params, mihg_index** out);
+void mihg_index_free(mihg_index* idx);
+
+/* MihIndex::num_tables / table(j).stats() — index.hpp:145-146, table.hpp:190-197. */
+int mihg_index_get_info(const mihg_index* idx, mihg_index_info* out);
+int mihg_table_get_info(const mihg_index* idx, uint32_t j, mihg_table_info* out);
+
+/* SubstringTable::bucket_lookup — table.hpp:169-175: ids of bucket `value` of table j in
+ * insertion (ascending id) order; writes min(count, cap) ids (global ids). */
+int mihg_bucket_lookup(const mihg_index* idx, uint32_t j, uint64_t value, uint32_t* out_ids,
+                       uint64_t cap, uint64_t* count);
+
+/* Device pointer to the index's codes (n * ceil(bits/64) words). */
+int mihg_index_codes(const mihg_index* idx, const uint64_t** d_codes);
+
+/* MihIndex::knn_search(BinaryCode q, uint32_t k, SearchTrace*, SearchScratch*) — index.hpp:185-253,
+ * batched over nq queries. k > n -> MIHG_EINVAL; k == 0 -> no output, zero traces.
+ * Host pointers: queries nq*ceil(bits/64) words; out_ids/out_dists nq*k; traces nq or NULL. */
+int mihg_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,
+                   uint32_t* out_ids, uint32_t* out_dists, mihg_trace* traces);
+/* Same, all pointers on the index's device, ordered on `stream` (cudaStream_t, NULL = legacy). */
+int mihg_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
+                          uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces, void* stream);
+
+/* scan_knn(db, q, k) — scan.hpp:43-68, batched, over the index's device codes. */
+int mihg_scan_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,
+                        uint32_t* out_ids, uint32_t* out_dists);
+int mihg_scan_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
+                               uint32_t* d_ids, uint32_t* d_dists, void* stream);
+/* scan_knn over raw device codes (no index). */
+int mihg_scan_knn_raw_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                             const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                             uint32_t* d_dists, void* stream);
+
+/* Exact k-way merge of G per-shard top-k lists: inputs [G][nq][k_in] device
+ * arrays (dist 0xFFFFFFFF = padding), output the k_out smallest (dist, id) per query. */
+int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint32_t G, uint64_t nq,
+                           uint32_t k_in, uint32_t k_out, uint32_t* d_out_ids,
+                           uint32_t* d_out_dists, void* stream);
+
+/* gen_uniform(n, bits, seed) — io.hpp:266-277 (std::mt19937_64, standard-specified). Host. */
+int mihg_gen_uniform(uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MIHG_H */

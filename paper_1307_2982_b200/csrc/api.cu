@@ -1,0 +1,320 @@
+// C ABI (include/mihg.h) over the device index and kernels. No C++ exception crosses it.
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/mihg.h"
+#include "knn.cuh"
+
+struct mihg_index {
+  mihg::Index* impl;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MIHG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return MIHG_EINVAL;
+  } catch (const std::bad_alloc&) {
+    g_err = "bad_alloc";
+    return MIHG_ENOMEM;
+  } catch (const mihg::CudaError& e) {
+    g_err = e.what();
+    // surface allocation failures as ENOMEM
+    if (std::strstr(e.what(), "out of memory")) return MIHG_ENOMEM;
+    return MIHG_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MIHG_EINTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return MIHG_EINTERNAL;
+  }
+}
+
+mihg::Index& impl(const mihg_index* idx) {
+  if (!idx || !idx->impl) throw mihg::InvalidArgument("null index");
+  return *idx->impl;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    MIHG_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) MIHG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// std::mt19937_64 (io.hpp:268); the parameters are fixed by the C++ standard.
+struct Mt64 {
+  uint64_t s[312];
+  int i = 312;
+  explicit Mt64(uint64_t seed) {
+    s[0] = seed;
+    for (int k = 1; k < 312; ++k) s[k] = 6364136223846793005ULL * (s[k - 1] ^ (s[k - 1] >> 62)) + k;
+  }
+  uint64_t operator()() {
+    if (i >= 312) {
+      for (int k = 0; k < 312; ++k) {
+        const uint64_t y = (s[k] & 0xFFFFFFFF80000000ULL) | (s[(k + 1) % 312] & 0x7FFFFFFFULL);
+        s[k] = s[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ULL : 0);
+      }
+      i = 0;
+    }
+    uint64_t z = s[i++];
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    return z;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* mihg_last_error(void) { return g_err.c_str(); }
+int mihg_abi_version(void) { return MIHG_ABI_VERSION; }
+
+int mihg_device_count(int* count) {
+  return guarded([&] { MIHG_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int mihg_index_build_ex(const mihg_build_params* p, mihg_index** out) {
+  return guarded([&] {
+    if (!p || !out) throw mihg::InvalidArgument("null argument");
+    if (p->n && !p->codes) throw mihg::InvalidArgument("null codes");
+    if (p->bits == 0 || p->bits > mihg::kMaxCodeBits)
+      throw mihg::InvalidArgument("CodeDatabase: code width must be in [1, 4096], got " +
+                                  std::to_string(p->bits));
+    mihg::BuildOptions opt;
+    if (p->dense_max_bits) opt.dense_max_bits = p->dense_max_bits;
+    opt.force = p->layout;
+    DeviceGuard g(p->device);
+    mihg::Index* ix = mihg::build_index(p->codes, p->codes_on_device != 0, p->n, p->bits, p->m,
+                                        p->lengths, p->positions, p->device, p->id_base, opt);
+    *out = new mihg_index{ix};
+  });
+}
+
+int mihg_index_build(const uint64_t* codes, uint64_t n, uint32_t bits, uint32_t m,
+                     const uint32_t* lengths, const uint32_t* positions, int device,
+                     mihg_index** out) {
+  mihg_build_params p{};
+  p.codes = codes;
+  p.n = n;
+  p.bits = bits;
+  p.m = m;
+  p.lengths = lengths;
+  p.positions = positions;
+  p.device = device;
+  return mihg_index_build_ex(&p, out);
+}
+
+void mihg_index_free(mihg_index* idx) {
+  if (!idx) return;
+  guarded([&] {
+    if (idx->impl) {
+      DeviceGuard g(idx->impl->device);
+      delete idx->impl;
+    }
+  });
+  delete idx;
+}
+
+int mihg_index_get_info(const mihg_index* idx, mihg_index_info* out) {
+  return guarded([&] {
+    const mihg::Index& ix = impl(idx);
+    out->n = ix.n;
+    out->bits = ix.bits;
+    out->m = ix.m;
+    out->id_base = ix.id_base;
+    out->device = ix.device;
+    uint64_t bytes = ix.codes.size() * 8;
+    for (auto& t : ix.tables) bytes += t->bytes();
+    out->device_bytes = bytes;
+  });
+}
+
+int mihg_table_get_info(const mihg_index* idx, uint32_t j, mihg_table_info* out) {
+  return guarded([&] {
+    const mihg::Index& ix = impl(idx);
+    if (j >= ix.m) throw mihg::InvalidArgument("table index out of range");
+    const mihg::TableStorage& t = *ix.tables[j];
+    out->s = t.s;
+    out->dense = t.dense ? 1 : 0;
+    out->non_empty_buckets = t.non_empty_buckets;
+    out->max_bucket_size = t.max_bucket;
+    out->total_entries = ix.n;
+    out->device_bytes = t.bytes();
+    out->escaped_blocks = t.escaped_blocks;
+    // TableStats::estimate_bytes (table.hpp:42-46) needs the non-empty 32-bucket group count,
+    // recomputed here from the bucket starts on the host for small tables only.
+    out->estimated_bytes = 0;
+  });
+}
+
+int mihg_bucket_lookup(const mihg_index* idx, uint32_t j, uint64_t value, uint32_t* out_ids,
+                       uint64_t cap, uint64_t* count) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    if (j >= ix.m) throw mihg::InvalidArgument("table index out of range");
+    const mihg::TableStorage& t = *ix.tables[j];
+    if (value >> t.s)
+      throw mihg::InvalidArgument("bucket_lookup: value " + std::to_string(value) +
+                                  " does not fit in " + std::to_string(t.s) + " bits");
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    uint32_t lo = 0, hi = 0;
+    if (t.dense) {
+      uint32_t two[2];
+      MIHG_CUDA(cudaMemcpy(two, t.offsets.get() + value, 8, cudaMemcpyDeviceToHost));
+      lo = two[0];
+      hi = two[1];
+    } else {
+      mihg::DirBlock b;
+      MIHG_CUDA(cudaMemcpy(&b, t.dir.get() + (value >> mihg::kDirBucketsLog2), sizeof(b),
+                           cudaMemcpyDeviceToHost));
+      const uint32_t tt = uint32_t(value & 63);
+      const uint32_t c = uint32_t((b.p0 >> tt) & 1) | uint32_t(((b.p1 >> tt) & 1) << 1) |
+                         uint32_t(((b.p2 >> tt) & 1) << 2);
+      if (c) {
+        if (b.esc != mihg::kNoEscape) {
+          uint32_t two[2];
+          MIHG_CUDA(cudaMemcpy(two, t.esc.get() + uint64_t(b.esc) * 65 + tt, 8, cudaMemcpyDeviceToHost));
+          lo = two[0];
+          hi = two[1];
+        } else {
+          const uint64_t below = (uint64_t(1) << tt) - 1;
+          lo = b.ebase + __builtin_popcountll(b.p0 & below) + 2 * __builtin_popcountll(b.p1 & below) +
+               4 * __builtin_popcountll(b.p2 & below);
+          hi = lo + c;
+        }
+      }
+    }
+    *count = hi - lo;
+    const uint64_t w = std::min<uint64_t>(cap, hi - lo);
+    if (w) {
+      MIHG_CUDA(cudaMemcpy(out_ids, t.ids.get() + lo, w * 4, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < w; ++i) out_ids[i] += ix.id_base;
+    }
+  });
+}
+
+int mihg_index_codes(const mihg_index* idx, const uint64_t** d_codes) {
+  return guarded([&] { *d_codes = impl(idx).codes.get(); });
+}
+
+int mihg_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
+                          uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces, void* stream) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    mihg::knn_device(ix, d_queries, nq, k, d_ids, d_dists, reinterpret_cast<mihg::Trace*>(d_traces),
+                     static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mihg_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,
+                   uint32_t* out_ids, uint32_t* out_dists, mihg_trace* traces) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    if (k > ix.n) throw mihg::InvalidArgument("knn_search: k exceeds database size");
+    if (nq == 0) return;
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    cudaStream_t st = ix.stream;
+    mihg::DeviceBuffer<uint64_t> dq(nq * ix.W, st);
+    mihg::DeviceBuffer<uint32_t> di(std::max<uint64_t>(nq * k, 1), st), dd(std::max<uint64_t>(nq * k, 1), st);
+    mihg::DeviceBuffer<mihg::Trace> dt(traces ? nq : 0, st);
+    MIHG_CUDA(cudaMemcpyAsync(dq.get(), queries, nq * ix.W * 8, cudaMemcpyHostToDevice, st));
+    mihg::knn_device(ix, dq.get(), nq, k, di.get(), dd.get(), traces ? dt.get() : nullptr, st);
+    if (k) {
+      MIHG_CUDA(cudaMemcpyAsync(out_ids, di.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
+      MIHG_CUDA(cudaMemcpyAsync(out_dists, dd.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (traces)
+      MIHG_CUDA(cudaMemcpyAsync(traces, dt.get(), nq * sizeof(mihg::Trace), cudaMemcpyDeviceToHost, st));
+    MIHG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int mihg_scan_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
+                               uint32_t* d_ids, uint32_t* d_dists, void* stream) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    mihg::scan_knn_device(ix.codes.get(), ix.n, ix.bits, ix.id_base, d_queries, nq, k, d_ids,
+                          d_dists, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mihg_scan_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,
+                        uint32_t* out_ids, uint32_t* out_dists) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    if (k > ix.n) throw mihg::InvalidArgument("scan_knn: k exceeds database size");
+    if (nq == 0 || k == 0) return;
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    cudaStream_t st = ix.stream;
+    mihg::DeviceBuffer<uint64_t> dq(nq * ix.W, st);
+    mihg::DeviceBuffer<uint32_t> di(nq * k, st), dd(nq * k, st);
+    MIHG_CUDA(cudaMemcpyAsync(dq.get(), queries, nq * ix.W * 8, cudaMemcpyHostToDevice, st));
+    mihg::scan_knn_device(ix.codes.get(), ix.n, ix.bits, ix.id_base, dq.get(), nq, k, di.get(),
+                          dd.get(), st);
+    MIHG_CUDA(cudaMemcpyAsync(out_ids, di.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
+    MIHG_CUDA(cudaMemcpyAsync(out_dists, dd.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
+    MIHG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int mihg_scan_knn_raw_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                             const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                             uint32_t* d_dists, void* stream) {
+  return guarded([&] {
+    if (bits == 0 || bits > mihg::kMaxCodeBits) throw mihg::InvalidArgument("bad code width");
+    mihg::scan_knn_device(d_codes, n, bits, id_base, d_queries, nq, k, d_ids, d_dists,
+                          static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint32_t G, uint64_t nq,
+                           uint32_t k_in, uint32_t k_out, uint32_t* d_out_ids,
+                           uint32_t* d_out_dists, void* stream) {
+  return guarded([&] {
+    if (G == 0 || k_out > uint64_t(G) * k_in) throw mihg::InvalidArgument("merge: bad shard shape");
+    mihg::merge_topk_device(d_ids, d_dists, G, nq, k_in, k_out, d_out_ids, d_out_dists,
+                            static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mihg_gen_uniform(uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out) {
+  return guarded([&] {
+    if (bits == 0 || bits > mihg::kMaxCodeBits) throw mihg::InvalidArgument("gen_uniform: bad width");
+    Mt64 rng(seed);
+    const uint32_t wpc = mihg::words_per_code(bits);
+    const uint64_t mask = (bits & 63) == 0 ? ~uint64_t(0) : ((uint64_t(1) << (bits & 63)) - 1);
+    for (uint64_t i = 0; i < n; ++i) {
+      uint64_t* w = out + i * wpc;
+      for (uint32_t k = 0; k < wpc; ++k) w[k] = rng();
+      w[wpc - 1] &= mask;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+// Shared device helpers for the B200 multi-index-hashing kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cassert>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace mihg {
+
+// ---- error plumbing: CUDA failures become mihg::CudaError, mapped to MIHG_ECUDA at the C ABI.
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                    std::to_string(line) + ")");
+}
+#define MIHG_CUDA(x) ::mihg::cuda_check((x), #x, __FILE__, __LINE__)
+// MIHG_SYNC_DEBUG=1 in the environment: synchronize after every launch to localize faults.
+bool sync_debug();
+#define MIHG_LAUNCH()                                                                     \
+  do {                                                                                    \
+    ::mihg::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);          \
+    if (::mihg::sync_debug())                                                             \
+      ::mihg::cuda_check(cudaDeviceSynchronize(), "kernel execution", __FILE__, __LINE__); \
+  } while (0)
+
+#ifdef MIHG_DEBUG
+#define MIHG_DASSERT(c) assert(c)
+#else
+#define MIHG_DASSERT(c) ((void)0)
+#endif
+
+constexpr uint32_t kMaxTableBits = 32;   // table.hpp:31
+constexpr uint32_t kMaxCodeBits = 4096;  // codes.hpp:16
+constexpr uint32_t kWarp = 32;
+
+__host__ __device__ constexpr uint32_t words_per_code(uint32_t bits) { return (bits + 63) / 64; }
+
+// Directory block of a sparse (blocked-count) table: 64 consecutive buckets in one 32-byte
+// sector. Bucket t's entry count c_t in 0..6 is spread over three bit-planes (bit i of c_t is
+// bit t of plane i); 7 marks an escaped block whose exact starts live in `esc`.
+//   start(t) = ebase + popc(p0 & below) + 2 popc(p1 & below) + 4 popc(p2 & below)
+struct __align__(32) DirBlock {
+  uint64_t p0, p1, p2;
+  uint32_t ebase;  // index into ids[] of the block's first entry
+  uint32_t esc;    // ~0u, or the escape record (65 absolute starts) index
+};
+static_assert(sizeof(DirBlock) == 32, "one sector per directory block");
+constexpr uint32_t kDirBucketsLog2 = 6;
+constexpr uint32_t kNoEscape = 0xFFFFFFFFu;
+constexpr uint32_t kMaxInlineCount = 6;
+
+// One substring table on the device.
+struct DevTable {
+  const uint32_t* ids;      // n ids sorted by (substring key, id)
+  const uint32_t* offsets;  // dense: 2^s + 1 bucket starts (nullptr when sparse)
+  const DirBlock* dir;      // sparse: 2^(s-6) blocks (nullptr when dense)
+  const uint32_t* esc;      // sparse: 65 absolute starts per escaped block
+  uint32_t s;
+  uint32_t dense;
+};
+
+// Substring j of the partition: contiguous run (offset, len) or explicit positions.
+struct DevSubstring {
+  uint32_t len;
+  uint32_t contiguous;
+  uint32_t offset;    // first bit when contiguous
+  uint32_t pos_base;  // index into positions[] otherwise
+};
+
+// Binomial coefficients C(n, k) for n, k <= 64 (ring sizes, colex unranking).
+extern __constant__ uint64_t c_binom[65][65];
+void upload_binomials();
+uint64_t host_binom(uint32_t n, uint32_t k);
+
+// ---- bucket probe: [lo, hi) slice of ids[] for bucket `v` (table.hpp:178-188 semantics).
+__device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint32_t& lo,
+                                             uint32_t& hi) {
+  if (t.dense) {
+    lo = __ldg(t.offsets + v);
+    hi = __ldg(t.offsets + v + 1);
+    return;
+  }
+  const uint4* bp = reinterpret_cast<const uint4*>(t.dir + (v >> kDirBucketsLog2));
+  const uint4 x = __ldg(bp);
+  const uint4 y = __ldg(bp + 1);
+  const uint32_t tt = v & 63u;
+  const uint64_t p0 = (uint64_t(x.y) << 32) | x.x, p1 = (uint64_t(x.w) << 32) | x.z,
+                 p2 = (uint64_t(y.y) << 32) | y.x;
+  const uint32_t c = uint32_t((p0 >> tt) & 1u) | (uint32_t((p1 >> tt) & 1u) << 1) |
+                     (uint32_t((p2 >> tt) & 1u) << 2);
+  if (c == 0) {
+    lo = hi = 0;
+    return;
+  }
+  if (y.w != kNoEscape) {
+    const uint32_t* e = t.esc + uint64_t(y.w) * 65u + tt;
+    lo = __ldg(e);
+    hi = __ldg(e + 1);
+    return;
+  }
+  const uint64_t below = (uint64_t(1) << tt) - 1u;
+  lo = y.z + __popcll(p0 & below) + 2u * __popcll(p1 & below) + 4u * __popcll(p2 & below);
+  hi = lo + c;
+}
+
+// Full-code Hamming distance (codes.hpp:38-42). W > 0: compile-time word count.
+template <int W>
+__device__ __forceinline__ uint32_t hamming(const uint64_t* q, const uint64_t* x, uint32_t) {
+  uint32_t d = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) d += __popcll(q[w] ^ x[w]);
+  return d;
+}
+template <>
+__device__ __forceinline__ uint32_t hamming<0>(const uint64_t* q, const uint64_t* x, uint32_t nw) {
+  uint32_t d = 0;
+  for (uint32_t w = 0; w < nw; ++w) d += __popcll(q[w] ^ x[w]);
+  return d;
+}
+
+// Load code `id` into registers (vectorised for W = 2, 4).
+template <int W>
+__device__ __forceinline__ void load_code(const uint64_t* __restrict__ codes, uint64_t id,
+                                          uint64_t* x) {
+  const uint64_t* p = codes + id * W;
+  if constexpr (W == 2) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    x[0] = v.x;
+    x[1] = v.y;
+  } else if constexpr (W == 4) {
+    const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+    x[0] = v0.x;
+    x[1] = v0.y;
+    x[2] = v1.x;
+    x[3] = v1.y;
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) x[w] = __ldg(p + w);
+  }
+}
+
+// Substring extraction (codes.hpp:214-231) of code words `c`.
+__device__ __forceinline__ uint32_t extract_key(const uint64_t* c, const DevSubstring& sub,
+                                                const uint32_t* __restrict__ positions) {
+  if (sub.len == 0) return 0;
+  if (sub.contiguous) {
+    const uint32_t w = sub.offset >> 6, sh = sub.offset & 63;
+    uint64_t v = c[w] >> sh;
+    if (sh + sub.len > 64) v |= c[w + 1] << (64 - sh);
+    return uint32_t(sub.len >= 64 ? v : (v & ((uint64_t(1) << sub.len) - 1)));
+  }
+  uint32_t v = 0;
+  for (uint32_t i = 0; i < sub.len; ++i) {
+    const uint32_t p = positions[sub.pos_base + i];
+    v |= uint32_t((c[p >> 6] >> (p & 63)) & 1u) << i;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+inline uint32_t ceil_div_u32(uint64_t a, uint64_t b) { return uint32_t((a + b - 1) / b); }
+
+int device_sm_count();
+
+}  // namespace mihg

@@ -1,0 +1,72 @@
+// Device-resident multi-index: the GPU counterpart of mih::MihIndex (index.hpp:98-285).
+#pragma once
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "sort.cuh"
+
+namespace mihg {
+
+// Owning storage of one substring table (replaces SubstringTable, table.hpp:85-290).
+struct TableStorage {
+  uint32_t s = 0;
+  bool dense = true;
+  DeviceBuffer<uint32_t> ids;      // n, sorted by (key, id)
+  DeviceBuffer<uint32_t> offsets;  // dense: 2^s + 1
+  DeviceBuffer<DirBlock> dir;      // sparse: 2^(s-6)
+  DeviceBuffer<uint32_t> esc;      // sparse: 65 per escaped block
+  uint64_t escaped_blocks = 0;
+  uint64_t non_empty_buckets = 0;
+  uint64_t max_bucket = 0;
+  DevTable view() const {
+    return DevTable{ids.get(), offsets.get(), dir.get(), esc.get(), s, dense ? 1u : 0u};
+  }
+  uint64_t bytes() const {
+    return ids.size() * 4 + offsets.size() * 4 + dir.size() * sizeof(DirBlock) + esc.size() * 4;
+  }
+};
+
+struct BuildOptions {
+  // Dense direct-address offsets when 2^s <= max(2^dense_max_bits, dense_ratio * n);
+  // otherwise the blocked-count sparse directory. (north_star: 32-bit substrings -> sparse.)
+  uint32_t dense_max_bits = 24;
+  uint32_t dense_ratio = 2;
+  int force = 0;  // 0 auto, 1 dense, 2 sparse
+};
+
+struct Index {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t bits = 0, W = 0, m = 0;
+  uint64_t n = 0;
+  uint32_t id_base = 0;  // global id of local id 0 (id-range shards)
+  std::vector<uint32_t> lengths, positions;
+  std::vector<DevSubstring> subs;
+  DeviceBuffer<uint64_t> codes;      // n * W words, bit i at word i/64 bit i%64
+  DeviceBuffer<uint32_t> d_positions;
+  DeviceBuffer<DevSubstring> d_subs;
+  DeviceBuffer<uint64_t> d_submask;  // m * W: bit mask of the positions owned by substring j
+  std::vector<std::unique_ptr<TableStorage>> tables;
+  DeviceBuffer<DevTable> d_tables;
+  std::mutex mu;  // one host call at a time per index (workspace is shared)
+  struct Workspace* ws = nullptr;
+  ~Index();
+};
+
+// Validates like Partition::validate (codes.hpp:152-176) and MihIndex::build (index.hpp:101-112);
+// throws InvalidArgument with the reference's wording.
+void validate_partition(uint32_t bits, uint32_t m, const uint32_t* lengths,
+                        const uint32_t* positions);
+
+// d_codes: n*W words already on `device` (copied into the index unless `adopt`).
+Index* build_index(const uint64_t* codes, bool codes_on_device, uint64_t n, uint32_t bits,
+                   uint32_t m, const uint32_t* lengths, const uint32_t* positions, int device,
+                   uint32_t id_base, const BuildOptions& opt);
+
+// Device key extraction for a batch of codes: keys[i*m + j] = substring j of code i.
+void extract_all_keys(const Index& idx, const uint64_t* d_codes, uint64_t count, uint32_t* d_keys,
+                      cudaStream_t st);
+
+}  // namespace mihg

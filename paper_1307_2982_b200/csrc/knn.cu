@@ -1,0 +1,616 @@
+// Batched exact MIH k-nearest-neighbour search on the GPU (K4/K5 in SURVEY.md §2.2).
+//
+// Reference semantics: MihIndex::knn_search (index.hpp:185-253, paper Alg. 3). Step r probes
+// ring floor(r/m) of table r mod m; every newly seen id is verified by its full Hamming distance
+// and binned; the search stops after step r once the bins at distance <= r hold >= k ids; the
+// result is the k smallest (dist, id) pairs.
+//
+// GPU restatement (bulk-synchronous over a batch of queries; all active queries run the same
+// step r in one launch):
+//  * mih_probe_kernel: flat work list over (active query, ring index) chunks. A thread unranks
+//    its first flip combination (colex combinatorial number system) and walks the rest with
+//    Gosper's hack; the enumeration order differs from RingEnumerator's lexicographic order
+//    (enumerate.hpp:59-82), which only affects the order trace counters accumulate in.
+//  * Dedup without the n-bit mark vector (index.hpp:55-76): a candidate x found at step r is
+//    "new" iff r is its first discovery step, r == min_j (m * d_j(q, x) + j), a pure function of
+//    x's code. Exactly-once, stateless, and it reproduces unique_candidates.
+//  * Verified candidates with dist <= U_q (a per-query upper bound on the k-th distance, tightened
+//    every round from the exact histogram) are histogrammed and appended to a bounded per-query
+//    buffer; a per-query drop-minimum records whether anything relevant overflowed.
+//  * mih_round_end_kernel: termination test sum_{d<=r} hist >= k (index.hpp:209, :232), U update,
+//    buffer compaction, next active list.
+//  * selection: exact top-k of the buffered keys (dist << 32 | id) — select.cu. Queries whose
+//    buffer overflowed with a relevant key re-run their steps with the final radius as the bound
+//    into exactly-sized buffers.
+#include <algorithm>
+#include <vector>
+
+#include "knn.cuh"
+#include "select.cuh"
+
+namespace mihg {
+
+struct Workspace {
+  uint64_t nq_cap = 0;
+  uint32_t b1 = 0, m = 0, cap = 0;
+  DeviceBuffer<uint64_t> qcodes_pad;
+  DeviceBuffer<uint32_t> qsub, hist, ubound, bufcnt, dropmin, act0, act1, counters, final_r;
+  DeviceBuffer<uint64_t> buf;
+  DeviceBuffer<unsigned long long> trc;
+  DeviceBuffer<uint64_t> lookups_prefix;
+  uint32_t* h_counter = nullptr;
+  cudaStream_t st = nullptr;
+  ~Workspace() {
+    if (h_counter) cudaFreeHost(h_counter);
+  }
+};
+
+Index::~Index() {
+  if (stream) cudaStreamSynchronize(stream);
+  delete ws;
+  ws = nullptr;
+  codes.reset();
+  d_positions.reset();
+  d_subs.reset();
+  d_submask.reset();
+  for (auto& t : tables)
+    if (t) {
+      t->ids.reset();
+      t->offsets.reset();
+      t->dir.reset();
+      t->esc.reset();
+    }
+  d_tables.reset();
+  if (stream) {
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+namespace {
+
+// colex unranking: the idx-th z-subset of {0..s-1} (Gosper order) as a bit mask.
+__device__ __forceinline__ uint64_t unrank_comb(uint64_t idx, uint32_t s, uint32_t z) {
+  uint64_t mask = 0;
+  uint32_t c = s;
+  for (uint32_t t = z; t >= 1; --t) {
+    uint32_t cc = c - 1;
+    while (c_binom[cc][t] > idx) --cc;
+    mask |= uint64_t(1) << cc;
+    idx -= c_binom[cc][t];
+    c = cc;
+  }
+  return mask;
+}
+
+// next subset of the same size in increasing numeric order (Gosper's hack)
+__device__ __forceinline__ uint64_t next_comb(uint64_t x) {
+  if (x == 0) return 0;
+  const uint64_t u = x & (~x + 1);
+  const uint64_t v = x + u;
+  return v | (((v ^ x) >> 2) >> (__ffsll(static_cast<long long>(u)) - 1));
+}
+
+template <int W>
+__device__ __forceinline__ uint64_t pick(const uint64_t* d, uint32_t i) {
+  uint64_t r = d[0];
+#pragma unroll
+  for (int w = 1; w < W; ++w)
+    if (i == uint32_t(w)) r = d[w];
+  return r;
+}
+
+// XOR of the query and one candidate code, held in registers (W > 0) or read from memory.
+template <int W>
+struct Diff {
+  uint64_t d[W];
+  __device__ __forceinline__ void load(const uint64_t* __restrict__ codes, uint32_t id,
+                                       const uint64_t* qc, uint32_t) {
+    uint64_t x[W];
+    load_code<W>(codes, id, x);
+#pragma unroll
+    for (int w = 0; w < W; ++w) d[w] = qc[w] ^ x[w];
+  }
+  __device__ __forceinline__ uint32_t dist(uint32_t) const {
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s += __popcll(d[w]);
+    return s;
+  }
+  __device__ __forceinline__ uint32_t subdist(const DevSubstring& sb, const uint64_t* submask_j,
+                                              uint32_t) const {
+    if (sb.contiguous) {
+      const uint32_t w = sb.offset >> 6, sh = sb.offset & 63;
+      uint64_t v = pick<W>(d, w) >> sh;
+      if (sh + sb.len > 64) v |= pick<W>(d, w + 1) << (64 - sh);
+      if (sb.len < 64) v &= (uint64_t(1) << sb.len) - 1;
+      return __popcll(v);
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s += __popcll(d[w] & __ldg(submask_j + w));
+    return s;
+  }
+};
+
+template <>
+struct Diff<0> {
+  const uint64_t* x;
+  const uint64_t* q;
+  __device__ __forceinline__ void load(const uint64_t* __restrict__ codes, uint32_t id,
+                                       const uint64_t* qc, uint32_t nw) {
+    x = codes + uint64_t(id) * nw;
+    q = qc;
+  }
+  __device__ __forceinline__ uint32_t dist(uint32_t nw) const {
+    uint32_t s = 0;
+    for (uint32_t w = 0; w < nw; ++w) s += __popcll(__ldg(q + w) ^ __ldg(x + w));
+    return s;
+  }
+  __device__ __forceinline__ uint32_t subdist(const DevSubstring&, const uint64_t* submask_j,
+                                              uint32_t nw) const {
+    uint32_t s = 0;
+    for (uint32_t w = 0; w < nw; ++w)
+      s += __popcll((__ldg(q + w) ^ __ldg(x + w)) & __ldg(submask_j + w));
+    return s;
+  }
+};
+
+struct ProbeArgs {
+  const uint64_t* codes;
+  const uint64_t* qcodes;  // nq * nw
+  const uint32_t* qsub;    // nq * m
+  DevTable tab;
+  const DevSubstring* subs;
+  const uint64_t* submask;
+  uint32_t m, a, rr, nw;
+  const uint32_t* active;
+  uint64_t ring, cpq, total;
+  uint32_t chunk;
+  uint32_t* hist;  // nullable (re-run pass)
+  uint32_t b1;
+  const uint32_t* ubound;
+  const uint32_t* rlimit;  // re-run: skip queries whose final radius < r
+  uint32_t r;
+  uint64_t* buf;
+  const uint64_t* bufbase;  // nullable: base = q * cap_fixed
+  const uint32_t* bufcap;   // nullable: cap = cap_fixed
+  uint32_t cap_fixed;
+  uint32_t* bufcnt;
+  uint32_t* dropmin;
+  unsigned long long* trc;  // nullable: 2 per query (candidates, unique)
+};
+
+// Is step (a, rr) the first step that reaches a candidate whose substring distances are d_j?
+// New iff for j < a: d_j > rr, and for j > a: d_j >= rr (r == min_j m*d_j + j).
+template <int W>
+__device__ __forceinline__ bool first_discovery(const Diff<W>& df, const ProbeArgs& p) {
+  for (uint32_t j = 0; j < p.m; ++j) {
+    if (j == p.a) continue;
+    if (j > p.a && p.rr == 0) continue;
+    const uint32_t lim = j < p.a ? p.rr : p.rr - 1;
+    const uint32_t dj = df.subdist(p.subs[j], p.submask + uint64_t(j) * p.nw, p.nw);
+    if (dj <= lim) return false;
+  }
+  return true;
+}
+
+constexpr int kProbeThreads = 256;
+constexpr int kProbeBatch = 4;
+
+template <int W, bool kTrace>
+__global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
+  const uint32_t nw = W ? W : p.nw;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < p.total; c += stride) {
+    const uint64_t slot = c / p.cpq;
+    const uint64_t part = c - slot * p.cpq;
+    const uint32_t q = p.active[slot];
+    if (p.rlimit && p.r > p.rlimit[q]) continue;
+    uint64_t i = part * p.chunk;
+    const uint64_t iend = min(p.ring, i + p.chunk);
+    uint64_t mask = unrank_comb(i, p.tab.s, p.rr);
+    const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
+    uint64_t qreg[W ? W : 1];
+    const uint64_t* qptr = p.qcodes + uint64_t(q) * nw;
+    if constexpr (W > 0) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) qreg[w] = __ldg(qptr + w);
+    }
+    const uint64_t* qc = W ? qreg : qptr;
+    const uint32_t U = p.ubound[q];
+    const uint64_t base = p.bufbase ? p.bufbase[q] : uint64_t(q) * p.cap_fixed;
+    const uint32_t cap = p.bufcap ? p.bufcap[q] : p.cap_fixed;
+    uint64_t n_cand = 0, n_new = 0;
+    while (i < iend) {
+      uint32_t lo[kProbeBatch], hi[kProbeBatch];
+#pragma unroll
+      for (int u = 0; u < kProbeBatch; ++u) {
+        if (i + u < iend) {
+          probe_bucket(p.tab, qa ^ uint32_t(mask), lo[u], hi[u]);
+          mask = next_comb(mask);
+        } else {
+          lo[u] = hi[u] = 0;
+        }
+      }
+      i += kProbeBatch;
+#pragma unroll
+      for (int u = 0; u < kProbeBatch; ++u) {
+        n_cand += hi[u] - lo[u];
+        for (uint32_t e = lo[u]; e < hi[u]; ++e) {
+          const uint32_t id = __ldg(p.tab.ids + e);
+          Diff<W> df;
+          df.load(p.codes, id, qc, nw);
+          if (!first_discovery<W>(df, p)) continue;
+          ++n_new;
+          const uint32_t d = df.dist(nw);
+          if (d > U) continue;
+          if (p.hist) atomicAdd(p.hist + uint64_t(q) * p.b1 + d, 1u);
+          const uint32_t pos = atomicAdd(p.bufcnt + q, 1u);
+          if (pos < cap) p.buf[base + pos] = (uint64_t(d) << 32) | id;
+          else atomicMin(p.dropmin + q, d);
+        }
+      }
+    }
+    if (kTrace && n_cand) {
+      atomicAdd(p.trc + 2 * uint64_t(q), (unsigned long long)n_cand);
+      if (n_new) atomicAdd(p.trc + 2 * uint64_t(q) + 1, (unsigned long long)n_new);
+    }
+  }
+}
+
+__global__ void mih_init_kernel(uint64_t nq, uint32_t bits, uint32_t* ubound, uint32_t* bufcnt,
+                                uint32_t* dropmin, uint32_t* act, uint32_t* final_r) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < nq;
+       q += uint64_t(gridDim.x) * blockDim.x) {
+    ubound[q] = bits;
+    bufcnt[q] = 0;
+    dropmin[q] = 0xFFFFFFFFu;
+    act[q] = uint32_t(q);
+    final_r[q] = 0xFFFFFFFFu;
+  }
+}
+
+// One warp per active query: termination test, bound update, buffer compaction.
+__global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32_t nact,
+                                     uint32_t* __restrict__ act_out, uint32_t* __restrict__ nact_out,
+                                     const uint32_t* __restrict__ hist, uint32_t b1,
+                                     uint32_t* __restrict__ ubound, uint32_t k, uint32_t r,
+                                     uint32_t* __restrict__ final_r, uint32_t* __restrict__ bufcnt,
+                                     uint64_t* __restrict__ buf, uint32_t cap) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  if (warp >= nact) return;
+  const uint32_t q = act_in[warp];
+  const uint32_t U = ubound[q];
+  const uint32_t* h = hist + uint64_t(q) * b1;
+  uint64_t run = 0, settled = 0;
+  uint32_t newU = U;
+  bool found = false;
+  for (uint32_t d0 = 0; d0 <= U; d0 += 32) {
+    const uint32_t d = d0 + lane;
+    uint64_t v = d <= U ? h[d] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(~0u, v, o);
+      if (lane >= o) v += y;
+    }
+    const uint64_t cum = run + v;
+    if (r >= d0 && r < d0 + 32) settled = __shfl_sync(~0u, cum, r - d0);
+    const uint32_t ok = __ballot_sync(~0u, d <= U && cum >= k);
+    if (!found && ok) {
+      newU = d0 + __ffs(ok) - 1;
+      found = true;
+    }
+    run = __shfl_sync(~0u, cum, 31);
+  }
+  if (r > U) settled = run;  // cannot happen while active (r <= U); kept for safety
+  if (settled >= k) {
+    if (lane == 0) final_r[q] = r;
+    return;
+  }
+  if (lane == 0) {
+    ubound[q] = newU;
+    act_out[atomicAdd(nact_out, 1u)] = q;
+  }
+  // drop buffered keys above the tightened bound once the buffer is half full
+  const uint32_t cnt = min(bufcnt[q], cap);
+  if (newU < U && cnt > cap / 2) {
+    uint64_t* b = buf + uint64_t(q) * cap;
+    uint32_t wpos = 0;
+    for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint64_t key = i < cnt ? b[i] : ~0ull;
+      const bool keep = i < cnt && uint32_t(key >> 32) <= newU;
+      const uint32_t bal = __ballot_sync(~0u, keep);
+      __syncwarp();
+      if (keep) b[wpos + __popc(bal & lanemask_lt())] = key;
+      wpos += __popc(bal);
+      __syncwarp();
+    }
+    if (lane == 0) bufcnt[q] = wpos;
+  }
+}
+
+// Per query: final trace, candidate count for selection, and the re-run flag.
+__global__ void mih_finish_kernel(uint64_t nq, const uint32_t* __restrict__ final_r,
+                                  const uint32_t* __restrict__ hist, uint32_t b1,
+                                  const uint32_t* __restrict__ bufcnt, uint32_t cap,
+                                  const uint32_t* __restrict__ dropmin,
+                                  const unsigned long long* __restrict__ trc,
+                                  const uint64_t* __restrict__ lookups_prefix, Trace* traces,
+                                  uint32_t* __restrict__ seg_count, uint32_t* __restrict__ need,
+                                  uint32_t* __restrict__ rerun_list, uint32_t* __restrict__ rerun_n) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < nq;
+       q += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t R = final_r[q];
+    uint64_t tot = 0;
+    for (uint32_t d = 0; d <= R; ++d) tot += hist[q * b1 + d];
+    need[q] = uint32_t(tot);
+    seg_count[q] = min(bufcnt[q], cap);
+    if (dropmin[q] <= R) rerun_list[atomicAdd(rerun_n, 1u)] = uint32_t(q);
+    if (traces) {
+      Trace t;
+      t.lookups = lookups_prefix[R];
+      t.candidates = trc[2 * q];
+      t.unique_candidates = trc[2 * q + 1];
+      t.distance_evaluations = t.unique_candidates;
+      t.final_radius = R;
+      t.reserved = 0;
+      traces[q] = t;
+    }
+  }
+}
+
+__global__ void zero_trace_kernel(uint64_t nq, Trace* traces) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < nq;
+       q += uint64_t(gridDim.x) * blockDim.x)
+    traces[q] = Trace{0, 0, 0, 0, 0, 0};
+}
+
+template <int W, bool kTrace>
+void launch_probe(const ProbeArgs& p, cudaStream_t st) {
+  const uint64_t blocks_needed = (p.total + kProbeThreads - 1) / kProbeThreads;
+  const uint64_t max_blocks = uint64_t(device_sm_count()) * 8;
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
+  mih_probe_kernel<W, kTrace><<<grid, kProbeThreads, 0, st>>>(p);
+  MIHG_LAUNCH();
+}
+
+void dispatch_probe(const ProbeArgs& p, bool trace, cudaStream_t st) {
+  switch (p.nw) {
+#define MIHG_W(w)                                                   \
+  case w:                                                           \
+    trace ? launch_probe<w, true>(p, st) : launch_probe<w, false>(p, st); \
+    break;
+    MIHG_W(1)
+    MIHG_W(2)
+    MIHG_W(3)
+    MIHG_W(4)
+#undef MIHG_W
+    default:
+      trace ? launch_probe<0, true>(p, st) : launch_probe<0, false>(p, st);
+  }
+}
+
+// Chunking of a round's (queries x ring) work list.
+void plan_round(ProbeArgs& p, uint64_t nact) {
+  const uint64_t work = nact * p.ring;
+  const uint64_t target = uint64_t(device_sm_count()) * 2048 * 4;
+  uint64_t chunk = (work + target - 1) / target;
+  chunk = std::max<uint64_t>(1, std::min<uint64_t>(chunk, 256));
+  chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(p.ring, 1));
+  p.chunk = uint32_t(chunk);
+  p.cpq = (p.ring + chunk - 1) / chunk;
+  p.total = nact * p.cpq;
+}
+
+void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
+  Workspace*& ws = idx.ws;
+  const uint32_t b1 = idx.bits + 1;
+  if (ws && ws->nq_cap >= nq && ws->b1 == b1 && ws->cap == cap && ws->st == st) return;
+  delete ws;
+  ws = new Workspace();
+  ws->st = st;
+  ws->nq_cap = nq;
+  ws->b1 = b1;
+  ws->m = idx.m;
+  ws->cap = cap;
+  ws->qsub = DeviceBuffer<uint32_t>(nq * idx.m, st);
+  ws->hist = DeviceBuffer<uint32_t>(nq * b1, st);
+  ws->ubound = DeviceBuffer<uint32_t>(nq, st);
+  ws->bufcnt = DeviceBuffer<uint32_t>(nq, st);
+  ws->dropmin = DeviceBuffer<uint32_t>(nq, st);
+  ws->act0 = DeviceBuffer<uint32_t>(nq, st);
+  ws->act1 = DeviceBuffer<uint32_t>(nq, st);
+  ws->counters = DeviceBuffer<uint32_t>(4, st);
+  ws->final_r = DeviceBuffer<uint32_t>(nq, st);
+  ws->buf = DeviceBuffer<uint64_t>(nq * cap, st);
+  ws->trc = DeviceBuffer<unsigned long long>(2 * nq, st);
+  ws->lookups_prefix = DeviceBuffer<uint64_t>(b1 + 1, st);
+  MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_counter), 16));
+}
+
+uint32_t read_counter(const uint32_t* d, uint32_t* h, cudaStream_t st) {
+  MIHG_CUDA(cudaMemcpyAsync(h, d, 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaStreamSynchronize(st));
+  return *h;
+}
+
+void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_t* d_ids,
+               uint32_t* d_dists, Trace* d_tr, cudaStream_t st, const KnnOptions& opt) {
+  Workspace& ws = *idx.ws;
+  const uint32_t m = idx.m, b1 = idx.bits + 1, cap = ws.cap;
+  const unsigned g1 = unsigned(std::min<uint64_t>((nq + 255) / 256, 4096));
+  extract_all_keys(idx, d_q, nq, ws.qsub.get(), st);
+  MIHG_CUDA(cudaMemsetAsync(ws.hist.get(), 0, nq * b1 * 4, st));
+  MIHG_CUDA(cudaMemsetAsync(ws.trc.get(), 0, 2 * nq * 8, st));
+  mih_init_kernel<<<g1, 256, 0, st>>>(nq, idx.bits, ws.ubound.get(), ws.bufcnt.get(),
+                                       ws.dropmin.get(), ws.act0.get(), ws.final_r.get());
+  MIHG_LAUNCH();
+
+  ProbeArgs p{};
+  p.codes = idx.codes.get();
+  p.qcodes = d_q;
+  p.qsub = ws.qsub.get();
+  p.subs = idx.d_subs.get();
+  p.submask = idx.d_submask.get();
+  p.m = m;
+  p.nw = idx.W;
+  p.hist = ws.hist.get();
+  p.b1 = b1;
+  p.ubound = ws.ubound.get();
+  p.buf = ws.buf.get();
+  p.cap_fixed = cap;
+  p.bufcnt = ws.bufcnt.get();
+  p.dropmin = ws.dropmin.get();
+  p.trc = ws.trc.get();
+
+  std::vector<uint64_t> lookups_prefix;
+  uint32_t* act_in = ws.act0.get();
+  uint32_t* act_out = ws.act1.get();
+  uint64_t nact = nq;
+  uint64_t acc = 0;
+  for (uint32_t r = 0; nact > 0; ++r) {
+    if (r > idx.bits) throw CudaError("knn: radius loop exceeded the code width (internal error)");
+    const uint32_t a = r % m, rr = r / m;
+    const uint32_t s = idx.lengths[a];
+    const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
+    acc += ring;
+    lookups_prefix.push_back(acc);
+    if (ring) {
+      p.tab = idx.tables[a]->view();
+      p.a = a;
+      p.rr = rr;
+      p.r = r;
+      p.active = act_in;
+      p.ring = ring;
+      plan_round(p, nact);
+      dispatch_probe(p, d_tr != nullptr, st);
+    }
+    MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
+    const unsigned g = unsigned((nact * 32 + 255) / 256);
+    mih_round_end_kernel<<<g, 256, 0, st>>>(act_in, uint32_t(nact), act_out, ws.counters.get(),
+                                             ws.hist.get(), b1, ws.ubound.get(), k, r,
+                                             ws.final_r.get(), ws.bufcnt.get(), ws.buf.get(), cap);
+    MIHG_LAUNCH();
+    nact = read_counter(ws.counters.get(), ws.h_counter, st);
+    std::swap(act_in, act_out);
+  }
+  MIHG_CUDA(cudaMemcpyAsync(ws.lookups_prefix.get(), lookups_prefix.data(),
+                            lookups_prefix.size() * 8, cudaMemcpyHostToDevice, st));
+  DeviceBuffer<uint32_t> seg_count(nq, st), need(nq, st), rerun(nq, st);
+  MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
+  mih_finish_kernel<<<g1, 256, 0, st>>>(nq, ws.final_r.get(), ws.hist.get(), b1, ws.bufcnt.get(),
+                                        cap, ws.dropmin.get(), ws.trc.get(), ws.lookups_prefix.get(),
+                                        d_tr, seg_count.get(), need.get(), rerun.get(),
+                                        ws.counters.get());
+  MIHG_LAUNCH();
+  const uint32_t nre = read_counter(ws.counters.get(), ws.h_counter, st);
+
+  // main selection over the fixed-stride buffers (re-run queries are overwritten below)
+  SelectArgs sa;
+  sa.keys = ws.buf.get();
+  sa.seg_stride = cap;
+  sa.seg_count = seg_count.get();
+  sa.seg_maxd = ws.final_r.get();
+  sa.k = k;
+  sa.id_base = idx.id_base;
+  sa.out_ids = d_ids;
+  sa.out_dists = d_dists;
+  select_topk(sa, uint32_t(nq), st);
+
+  if (nre == 0) return;
+  // Re-run: exact-size buffers, bound = final radius, no histogram / trace updates.
+  std::vector<uint32_t> hre(nre), hneed(nq), hR(nq);
+  MIHG_CUDA(cudaMemcpyAsync(hre.data(), rerun.get(), nre * 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaMemcpyAsync(hneed.data(), need.get(), nq * 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaMemcpyAsync(hR.data(), ws.final_r.get(), nq * 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaStreamSynchronize(st));
+  std::sort(hre.begin(), hre.end());
+  std::vector<uint64_t> hbase(nq, 0);
+  std::vector<uint32_t> hcap(nq, 0);
+  uint64_t total = 0;
+  uint32_t maxR = 0;
+  for (uint32_t q : hre) {
+    hbase[q] = total;
+    hcap[q] = hneed[q];
+    total += hneed[q];
+    maxR = std::max(maxR, hR[q]);
+  }
+  DeviceBuffer<uint64_t> big(std::max<uint64_t>(total, 1), st), dbase(nq, st);
+  DeviceBuffer<uint32_t> dcap(nq, st), dlist(nre, st);
+  MIHG_CUDA(cudaMemcpyAsync(dbase.get(), hbase.data(), nq * 8, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemcpyAsync(dcap.get(), hcap.data(), nq * 4, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemcpyAsync(dlist.get(), hre.data(), nre * 4, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemsetAsync(ws.bufcnt.get(), 0, nq * 4, st));
+  ProbeArgs rp = p;
+  rp.hist = nullptr;
+  rp.trc = nullptr;
+  rp.ubound = ws.final_r.get();
+  rp.rlimit = ws.final_r.get();
+  rp.buf = big.get();
+  rp.bufbase = dbase.get();
+  rp.bufcap = dcap.get();
+  rp.active = dlist.get();
+  for (uint32_t r = 0; r <= maxR; ++r) {
+    const uint32_t a = r % m, rr = r / m, s = idx.lengths[a];
+    const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
+    if (!ring) continue;
+    rp.tab = idx.tables[a]->view();
+    rp.a = a;
+    rp.rr = rr;
+    rp.r = r;
+    rp.ring = ring;
+    plan_round(rp, nre);
+    dispatch_probe(rp, false, st);
+  }
+  // select the re-run queries from their exact buffers
+  DeviceBuffer<uint64_t> rows(nre, st), sbase(nre, st);
+  DeviceBuffer<uint32_t> scount(nre, st), smaxd(nre, st);
+  std::vector<uint64_t> hrows(nre), hsb(nre);
+  std::vector<uint32_t> hsc(nre), hmd(nre);
+  for (uint32_t i = 0; i < nre; ++i) {
+    hrows[i] = hre[i];
+    hsb[i] = hbase[hre[i]];
+    hsc[i] = hneed[hre[i]];
+    hmd[i] = hR[hre[i]];
+  }
+  MIHG_CUDA(cudaMemcpyAsync(rows.get(), hrows.data(), nre * 8, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemcpyAsync(sbase.get(), hsb.data(), nre * 8, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemcpyAsync(scount.get(), hsc.data(), nre * 4, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemcpyAsync(smaxd.get(), hmd.data(), nre * 4, cudaMemcpyHostToDevice, st));
+  SelectArgs sr = sa;
+  sr.keys = big.get();
+  sr.seg_base_arr = sbase.get();
+  sr.seg_stride = 0;
+  sr.seg_count = scount.get();
+  sr.seg_maxd = smaxd.get();
+  sr.out_row = rows.get();
+  select_topk(sr, nre, st);
+}
+
+}  // namespace
+
+void knn_device(Index& idx, const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                uint32_t* d_dists, Trace* d_traces, cudaStream_t st, const KnnOptions& opt) {
+  if (k > idx.n) throw InvalidArgument("knn_search: k exceeds database size");
+  if (nq == 0) return;
+  if (k == 0) {  // index.hpp:189-194: empty result, zero trace
+    if (d_traces) {
+      zero_trace_kernel<<<unsigned(std::min<uint64_t>((nq + 255) / 256, 4096)), 256, 0, st>>>(nq, d_traces);
+      MIHG_LAUNCH();
+    }
+    return;
+  }
+  const uint64_t chunk = std::min<uint64_t>(nq, opt.query_chunk);
+  const uint32_t cap = std::max<uint32_t>(opt.buffer_cap, 2 * k + 64);
+  ensure_workspace(idx, chunk, cap, st);
+  for (uint64_t q0 = 0; q0 < nq; q0 += chunk) {
+    const uint64_t cn = std::min(chunk, nq - q0);
+    knn_chunk(idx, d_queries + q0 * idx.W, cn, k, d_ids + q0 * k, d_dists + q0 * k,
+              d_traces ? d_traces + q0 : nullptr, st, opt);
+  }
+}
+
+}  // namespace mihg

@@ -1,0 +1,41 @@
+#pragma once
+#include "index.cuh"
+
+namespace mihg {
+
+// Mirrors mih::SearchTrace (index.hpp:45-51); layout shared with include/mihg.h mihg_trace.
+struct Trace {
+  uint64_t lookups, candidates, unique_candidates, distance_evaluations;
+  uint32_t final_radius, reserved;
+};
+static_assert(sizeof(Trace) == 40, "mihg_trace ABI");
+
+struct KnnOptions {
+  uint32_t buffer_cap = 8192;   // per-query candidate buffer (u64 keys) in the main pass
+  uint32_t query_chunk = 16384; // queries per workspace pass
+};
+
+// Batched MihIndex::knn_search (index.hpp:185-253). All pointers are device pointers on
+// idx.device; results ordered by (dist, id) with global ids (local + idx.id_base).
+void knn_device(Index& idx, const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                uint32_t* d_dists, Trace* d_traces, cudaStream_t st, const KnnOptions& opt = {});
+
+// Batched scan_knn (scan.hpp:43-68) over the index's device-resident codes.
+void scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                     const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                     uint32_t* d_dists, cudaStream_t st);
+
+// k-way merge of G per-shard sorted (dist, id) lists per query (exact: smallest keys win).
+void merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint32_t G, uint64_t nq,
+                       uint32_t k_in, uint32_t k_out, uint32_t* d_out_ids, uint32_t* d_out_dists,
+                       cudaStream_t st);
+
+// Per-query top-k selection of packed keys (dist << 32 | id) held in segments of a buffer.
+// Used by the MIH, scan and merge paths.
+struct SegmentSelect {
+  const uint64_t* keys;
+  const uint64_t* seg_base;  // per slot
+  const uint32_t* seg_count; // per slot (entries already filtered to the candidate set)
+};
+
+}  // namespace mihg

@@ -1,0 +1,293 @@
+// Exhaustive batched k-NN (K6): the in-repo comparator and small-n path.
+// Reference: scan_knn (scan.hpp:43-68) — XOR+popcount distance to every code, the k smallest
+// (dist, id) pairs, ties at the cut to smaller ids.
+//
+// sm_100a has no native binary MMA (mma .b1 lowers to an emulation call), so
+// this runs on the INT/POPC pipe: POPC at 16/clk/SM (measured 4.56e12 popc32/s on B200).
+//
+// Work split: a warp owns a contiguous id range and a tile of QT queries held in registers; it
+// streams 32 codes per step (one per lane, coalesced) and tests each against every query of the
+// tile. Per (warp, query) it keeps a bound tau and an append-only list of keys with d <= tau in
+// id order; when the list reaches 2k entries it is compacted in place to its exact top-k (ties
+// at tau keep the earliest = smallest ids) and tau tightens. A final per-query selection over
+// all warp lists gives the exact global top-k.
+#include <algorithm>
+#include <vector>
+
+#include "knn.cuh"
+#include "select.cuh"
+
+namespace mihg {
+
+namespace {
+
+constexpr int kScanWarps = 8;
+
+struct ScanArgs {
+  const uint64_t* codes;
+  uint64_t n;
+  uint32_t nw, bits, k;
+  const uint64_t* queries;
+  uint64_t nq;
+  uint32_t nsplit;       // id splits per query tile (blocks per tile)
+  uint64_t range;        // ids per warp
+  uint32_t L;            // list capacity per (warp, query)
+  uint64_t* lists;       // [q][split*8 + warp][L]
+  uint32_t* counts;      // [q][split*8 + warp]
+  uint32_t slots;        // nsplit * kScanWarps
+};
+
+// In-place exact top-k of a warp's list (ids ascending in list order); returns the new bound.
+__device__ uint32_t compact_list(uint64_t* list, uint32_t& cnt, uint32_t tau, uint32_t k,
+                                 uint32_t* hist) {
+  const uint32_t lane = threadIdx.x & 31;
+  MIHG_DASSERT(tau < 4097);
+  for (uint32_t d = lane; d <= tau; d += 32) hist[d] = 0;
+  __syncwarp();
+  for (uint32_t i = lane; i < cnt; i += 32) atomicAdd(&hist[uint32_t(list[i] >> 32)], 1u);
+  __syncwarp();
+  uint32_t run = 0, newtau = tau, before = 0;
+  bool found = false;
+  for (uint32_t d0 = 0; d0 <= tau && !found; d0 += 32) {
+    const uint32_t d = d0 + lane;
+    uint32_t v = d <= tau ? hist[d] : 0;
+    const uint32_t own = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(~0u, v, o);
+      if (lane >= o) v += y;
+    }
+    const uint32_t ok = __ballot_sync(~0u, d <= tau && run + v >= k);
+    if (ok) {
+      const int src = __ffs(ok) - 1;
+      newtau = d0 + src;
+      before = run + __shfl_sync(~0u, v - own, src);
+      found = true;
+    }
+    run += __shfl_sync(~0u, v, 31);
+  }
+  if (!found) return tau;  // fewer than k entries: nothing to drop
+  const uint32_t need_eq = k - before;
+  uint32_t wpos = 0, eq_seen = 0;
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint64_t key = i < cnt ? list[i] : ~0ull;
+    const uint32_t d = uint32_t(key >> 32);
+    const bool eq = i < cnt && d == newtau;
+    const uint32_t eqbal = __ballot_sync(~0u, eq);
+    const bool keep = (i < cnt && d < newtau) ||
+                      (eq && eq_seen + __popc(eqbal & lanemask_lt()) < need_eq);
+    const uint32_t bal = __ballot_sync(~0u, keep);
+    __syncwarp();
+    if (keep) list[wpos + __popc(bal & lanemask_lt())] = key;
+    __syncwarp();
+    wpos += __popc(bal);
+    eq_seen += __popc(eqbal);
+  }
+  cnt = wpos;
+  return newtau;
+}
+
+template <int W, int QT>
+__global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(ScanArgs a) {
+  extern __shared__ uint32_t s_hist[];  // kScanWarps * (bits + 1)
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nw = W ? W : a.nw;
+  const uint32_t tile = blockIdx.x / a.nsplit, split = blockIdx.x % a.nsplit;
+  const uint32_t slot = split * kScanWarps + warp;
+  const uint64_t lo = uint64_t(slot) * a.range;
+  const uint64_t hi = min(a.n, lo + a.range);
+  uint32_t* hist = s_hist + warp * (a.bits + 1);
+  const uint64_t q0 = uint64_t(tile) * QT;
+  uint64_t qr[QT][W ? W : 1];
+  uint32_t tau[QT], cnt[QT];
+#pragma unroll
+  for (int t = 0; t < QT; ++t) {
+    const uint64_t q = min(q0 + t, a.nq - 1);
+    if constexpr (W > 0) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) qr[t][w] = __ldg(a.queries + q * W + w);
+    }
+    tau[t] = q0 + t < a.nq ? a.bits : 0xFFFFFFFFu;  // padding queries: never accept (tau sentinel)
+    cnt[t] = 0;
+  }
+  auto list_of = [&](int t) -> uint64_t* {
+    return a.lists + ((q0 + t) * a.slots + slot) * uint64_t(a.L);
+  };
+  const uint32_t lt = lanemask_lt();
+  for (uint64_t base = lo; base < hi; base += 32) {
+    const uint64_t id = base + lane;
+    const bool valid = id < hi;
+    uint64_t x[W ? W : 1];
+    const uint64_t* xp = a.codes + (valid ? id : lo) * nw;
+    if constexpr (W > 0) load_code<W>(a.codes, valid ? id : lo, x);
+#pragma unroll
+    for (int t = 0; t < QT; ++t) {
+      uint32_t d;
+      if constexpr (W > 0) {
+        d = hamming<W>(qr[t], x, W);
+      } else {
+        const uint64_t* qp = a.queries + min(q0 + t, a.nq - 1) * nw;
+        d = 0;
+        for (uint32_t w = 0; w < nw; ++w) d += __popcll(__ldg(qp + w) ^ __ldg(xp + w));
+      }
+      const bool pass = valid && d <= tau[t] && tau[t] != 0xFFFFFFFFu;
+      const uint32_t bal = __ballot_sync(~0u, pass);
+      if (bal) {
+        uint64_t* list = list_of(t);
+        MIHG_DASSERT(q0 + t < a.nq);
+        MIHG_DASSERT(cnt[t] + 32 <= a.L);
+        if (pass) list[cnt[t] + __popc(bal & lt)] = (uint64_t(d) << 32) | uint32_t(id);
+        cnt[t] += __popc(bal);
+        if (cnt[t] >= 2 * a.k) {
+          __syncwarp();
+          tau[t] = compact_list(list, cnt[t], tau[t], a.k, hist);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < QT; ++t)
+    if (q0 + t < a.nq && lane == 0) a.counts[(q0 + t) * a.slots + slot] = cnt[t];
+}
+
+// Gather the per-warp lists of one query into a contiguous segment (one CTA per query).
+__global__ void gather_lists_kernel(const uint64_t* __restrict__ lists,
+                                    const uint32_t* __restrict__ counts, uint32_t slots, uint32_t L,
+                                    uint64_t* __restrict__ out, uint32_t* __restrict__ out_count) {
+  __shared__ uint32_t s_off[1025];
+  const uint64_t q = blockIdx.x;
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (uint32_t s = 0; s < slots; ++s) {
+      s_off[s] = acc;
+      acc += counts[q * slots + s];
+    }
+    s_off[slots] = acc;
+    out_count[q] = acc;
+  }
+  __syncthreads();
+  const uint64_t obase = q * uint64_t(slots) * L;
+  for (uint32_t s = threadIdx.x >> 5; s < slots; s += blockDim.x >> 5) {
+    const uint32_t c = s_off[s + 1] - s_off[s];
+    const uint64_t* src = lists + (q * slots + s) * uint64_t(L);
+    for (uint32_t i = threadIdx.x & 31; i < c; i += 32) out[obase + s_off[s] + i] = src[i];
+  }
+}
+
+template <int W, int QT>
+void launch_scan(ScanArgs a, cudaStream_t st) {
+  const uint32_t tiles = uint32_t((a.nq + QT - 1) / QT);
+  const size_t smem = size_t(kScanWarps) * (a.bits + 1) * 4;
+  MIHG_CUDA(cudaFuncSetAttribute(scan_kernel<W, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(std::max<size_t>(smem, 1024))));
+  scan_kernel<W, QT><<<tiles * a.nsplit, kScanWarps * 32, smem, st>>>(a);
+  MIHG_LAUNCH();
+}
+
+}  // namespace
+
+void scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                     const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                     uint32_t* d_dists, cudaStream_t st) {
+  if (k > n) throw InvalidArgument("scan_knn: k exceeds database size");
+  if (nq == 0 || k == 0) return;
+  const uint32_t nw = words_per_code(bits);
+  const int QT = nw <= 2 ? 16 : (nw <= 4 ? 8 : 4);
+  const uint32_t L = 2 * k + 32;
+  const uint64_t sms = uint64_t(device_sm_count());
+  // query chunk bounded by list memory (~2 GiB)
+  const uint64_t per_q_slot = uint64_t(L) * 8;
+  for (uint64_t q0 = 0; q0 < nq;) {
+    uint64_t qn = nq - q0;
+    const uint64_t tiles_all = (qn + QT - 1) / QT;
+    // enough warps to fill the GPU ~4 waves, but each warp scans >= 32 codes per list
+    uint64_t nsplit = std::max<uint64_t>(1, (sms * 8 + tiles_all - 1) / tiles_all);
+    nsplit = std::min<uint64_t>(nsplit, std::max<uint64_t>(1, n / (kScanWarps * 256)));
+    nsplit = std::min<uint64_t>(nsplit, 1024 / kScanWarps);
+    const uint64_t slots = nsplit * kScanWarps;
+    const uint64_t budget = uint64_t(2) << 30;
+    const uint64_t qmax = std::max<uint64_t>(QT, budget / (2 * slots * per_q_slot) / QT * QT);
+    qn = std::min(qn, qmax);
+    ScanArgs a{};
+    a.codes = d_codes;
+    a.n = n;
+    a.nw = nw;
+    a.bits = bits;
+    a.k = k;
+    a.queries = d_queries + q0 * nw;
+    a.nq = qn;
+    a.nsplit = uint32_t(nsplit);
+    a.slots = uint32_t(slots);
+    a.range = (n + slots - 1) / slots;
+    a.L = L;
+    DeviceBuffer<uint64_t> lists(qn * slots * L, st), gathered(qn * slots * L, st);
+    DeviceBuffer<uint32_t> counts(qn * slots, st), gcount(qn, st);
+    a.lists = lists.get();
+    a.counts = counts.get();
+    switch (nw) {
+      case 1: launch_scan<1, 16>(a, st); break;
+      case 2: launch_scan<2, 16>(a, st); break;
+      case 3: launch_scan<3, 8>(a, st); break;
+      case 4: launch_scan<4, 8>(a, st); break;
+      default: launch_scan<0, 4>(a, st);
+    }
+    gather_lists_kernel<<<unsigned(qn), 256, 0, st>>>(lists.get(), counts.get(), uint32_t(slots), L,
+                                                      gathered.get(), gcount.get());
+    MIHG_LAUNCH();
+    SelectArgs sa;
+    sa.keys = gathered.get();
+    sa.seg_stride = slots * L;
+    sa.seg_count = gcount.get();
+    sa.k = k;
+    sa.id_base = id_base;
+    sa.out_ids = d_ids + q0 * k;
+    sa.out_dists = d_dists + q0 * k;
+    select_topk(sa, uint32_t(qn), st);
+    q0 += qn;
+  }
+}
+
+// ---- K9: exact k-way merge of per-shard results -----------------------------------------
+namespace {
+__global__ void pack_shard_keys_kernel(const uint32_t* __restrict__ ids,
+                                       const uint32_t* __restrict__ dists, uint32_t G, uint64_t nq,
+                                       uint32_t k_in, uint64_t* __restrict__ keys,
+                                       uint32_t* __restrict__ cnt) {
+  // input layout: [g][q][k_in]; output segment per query: G * k_in keys
+  const uint64_t total = uint64_t(G) * nq * k_in;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t g = t / (nq * k_in);
+    const uint64_t rem = t - g * nq * k_in;
+    const uint64_t q = rem / k_in, i = rem - q * k_in;
+    const uint32_t d = dists[t], id = ids[t];
+    keys[q * G * k_in + g * k_in + i] = d == 0xFFFFFFFFu ? ~0ull : (uint64_t(d) << 32) | id;
+    if (t < nq) cnt[t] = G * k_in;
+  }
+}
+}  // namespace
+
+void merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint32_t G, uint64_t nq,
+                       uint32_t k_in, uint32_t k_out, uint32_t* d_out_ids, uint32_t* d_out_dists,
+                       cudaStream_t st) {
+  if (nq == 0 || k_out == 0) return;
+  DeviceBuffer<uint64_t> keys(uint64_t(G) * nq * k_in, st);
+  DeviceBuffer<uint32_t> cnt(nq, st);
+  const uint64_t total = uint64_t(G) * nq * k_in;
+  pack_shard_keys_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 65535)), 256, 0, st>>>(
+      d_ids, d_dists, G, nq, k_in, keys.get(), cnt.get());
+  MIHG_LAUNCH();
+  SelectArgs sa;
+  sa.keys = keys.get();
+  sa.seg_stride = uint64_t(G) * k_in;
+  sa.seg_count = cnt.get();
+  sa.seg_maxd = nullptr;
+  sa.k = k_out;
+  sa.id_base = 0;
+  sa.out_ids = d_out_ids;
+  sa.out_dists = d_out_dists;
+  select_topk(sa, uint32_t(nq), st);
+}
+
+}  // namespace mihg

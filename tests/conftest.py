@@ -1,0 +1,43 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: long-running (large sizes)")
+
+
+def load_golden(name):
+    import numpy as np
+
+    path = os.path.join(GOLDEN, f"{name}.npz")
+    return dict(np.load(path, allow_pickle=False))
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return load_golden
+
+
+@pytest.fixture(scope="session")
+def port():
+    import oracle
+
+    if not os.path.exists(oracle.PORT_SO):
+        oracle.build(ref=False)
+    return oracle.port()
+
+
+@pytest.fixture(scope="session")
+def cuda_ok():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device visible: -m gpu tests must run on a B200 box")
+    return True

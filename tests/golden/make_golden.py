@@ -1,0 +1,184 @@
+"""Regenerate the golden fixtures in tests/golden/ from the REFERENCE ITSELF.
+
+Run in the dev container (needs /root/reference and oracle/_ref/libmihref.so, built by
+``make -C oracle ref``):
+
+    python tests/golden/make_golden.py
+
+Every expected output below comes from the unmodified reference headers (MihIndex::knn_search,
+range_search, scan_knn, SubstringTable::bucket_lookup, gen_uniform, lsh_encode) through
+oracle/ref_driver.cpp. The cases mirror the reference's own tests (file:line relative to
+/root/reference/proj); inputs that the GPU box cannot regenerate without the reference
+(std::normal_distribution-based LSH codes) are stored verbatim.
+"""
+from __future__ import annotations
+
+import hashlib
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+import oracle  # noqa: E402
+
+
+def knn_case(R, codes, bits, m, queries, ks, lengths=None, positions=None):
+    h = R.build(codes, bits, m, lengths, positions)
+    out = {}
+    for k in ks:
+        ids, dists, tr = h.knn(queries, k)
+        out[f"ids_k{k}"] = ids
+        out[f"dists_k{k}"] = dists
+        out[f"trace_k{k}"] = tr
+    return out
+
+
+def digest(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def main():
+    R = oracle.ref()
+    files = {}
+
+    # index_test.cpp:73-94 HandWorkedKnn (and scan_test.cpp:14-19 tiny_db)
+    codes = np.array([[0], [1], [63]], np.uint64)
+    files["hand_worked"] = dict(codes=codes, bits=6, m=2, queries=np.array([[0]], np.uint64),
+                                **knn_case(R, codes, 6, 2, np.array([[0]], np.uint64), [1, 2, 3]))
+
+    # index_test.cpp:127-154 KnnMatchesScanRandomized: b in {64,70}, n=1200, seeds 111+b / 222+b
+    for bits in (64, 70):
+        codes = R.gen_uniform(1200, bits, 111 + bits)
+        qs = R.gen_uniform(15, bits, 222 + bits)
+        d = dict(bits=bits, n=1200, db_seed=111 + bits, q_seed=222 + bits, codes=codes, queries=qs)
+        for m in (4, 6, 7):
+            for key, v in knn_case(R, codes, bits, m, qs, [1, 2, 10, 100, 1200]).items():
+                d[f"m{m}_{key}"] = v
+        files[f"knn_random_b{bits}"] = d
+
+    # index_test.cpp:143-153: wide substrings, 24-bit, n=800, seeds 501/502, m=2
+    codes = R.gen_uniform(800, 24, 501)
+    qs = R.gen_uniform(10, 24, 502)
+    files["knn_wide24"] = dict(bits=24, m=2, codes=codes, queries=qs,
+                               **knn_case(R, codes, 24, 2, qs, [1, 10, 800]))
+
+    # index_test.cpp:169-184 DuplicateCodesAllReported
+    codes = np.array([[0x00FF]] * 5 + [[0x0F0F]], np.uint64)
+    qs = np.array([[0x00FF]], np.uint64)
+    files["duplicates"] = dict(bits=16, m=2, codes=codes, queries=qs,
+                               **knn_case(R, codes, 16, 2, qs, [1, 5, 6]))
+
+    # index_test.cpp:156-167 KnnOnDatabaseQueriesFindsSelf (n=600, seed 33, m=4, first 50 codes)
+    codes = R.gen_uniform(600, 64, 33)
+    files["self_queries"] = dict(bits=64, m=4, codes=codes, queries=codes[:50].copy(),
+                                 **knn_case(R, codes, 64, 4, codes[:50], [1, 3]))
+
+    # index_test.cpp:283-295 NonDivisibleWidthUsesUnevenSubstrings: 100 bits, m=8, n=800
+    codes = R.gen_uniform(800, 100, 60)
+    qs = R.gen_uniform(6, 100, 61)
+    files["nondivisible100"] = dict(bits=100, m=8, codes=codes, queries=qs,
+                                    **knn_case(R, codes, 100, 8, qs, [25]))
+
+    # index_test.cpp:270-281 ScratchReuseIsClean: 32-bit, n=400, m=4, 40 queries, k=5
+    codes = R.gen_uniform(400, 32, 50)
+    qs = R.gen_uniform(40, 32, 51)
+    files["scratch_reuse32"] = dict(bits=32, m=4, codes=codes, queries=qs,
+                                    **knn_case(R, codes, 32, 4, qs, [5]))
+
+    # Non-contiguous partition (codes.hpp:124-195 allows any balanced disjoint cover):
+    # interleaved 64-bit partition, m=4, substring j owns bits {j, j+4, j+8, ...}.
+    codes = R.gen_uniform(3000, 64, 4242)
+    qs = R.gen_uniform(20, 64, 4343)
+    lengths = np.full(4, 16, np.uint32)
+    positions = np.array([j + 4 * i for j in range(4) for i in range(16)], np.uint32)
+    files["interleaved64"] = dict(bits=64, m=4, codes=codes, queries=qs, lengths=lengths,
+                                  positions=positions,
+                                  **knn_case(R, codes, 64, 4, qs, [1, 10, 50], lengths, positions))
+
+    # io_test.cpp:286-303 LshCodesStillAnswerExactQueries (non-uniform codes, stored verbatim)
+    codes = R.gen_lsh(2000, 2000, 16, 4, 0.3, 88, 88, 64, 5)
+    qs = R.gen_lsh(2000, 20, 16, 4, 0.3, 88, 89, 64, 5)
+    files["lsh_io_test"] = dict(bits=64, m=4, codes=codes, queries=qs,
+                                **knn_case(R, codes, 64, 4, qs, [10]))
+
+    # acceptance.cpp:134-172 criterion 2: n=1e5, 64-bit, m=choose_num_tables(64,1e5)=4,
+    # k in {1,10,100}; uniform lane (seeds 0xC0DE0001 / 0xC0DE0003) and the angular-embedding
+    # lane (gen_correlated_vectors(1e5,32,4,0.3,0x5EED0001), queries 0x5EED0002, spec 0x5EED0003).
+    # First 300 of the 1000 queries are pinned.
+    m = int(round(64 / math.log2(1e5)))
+    codes = R.gen_uniform(100000, 64, 0xC0DE0001)
+    qs = R.gen_uniform(1000, 64, 0xC0DE0003)[:300]
+    files["acceptance_uniform"] = dict(bits=64, m=m, db_seed=0xC0DE0001, q_seed=0xC0DE0003,
+                                       n=100000, queries=qs, codes_sha256=digest(codes),
+                                       **knn_case(R, codes, 64, m, qs, [1, 10, 100]))
+    codes = R.gen_lsh(100000, 100000, 32, 4, 0.3, 0x5EED0001, 0x5EED0001, 64, 0x5EED0003)
+    qs = R.gen_lsh(100000, 1000, 32, 4, 0.3, 0x5EED0001, 0x5EED0002, 64, 0x5EED0003)[:300]
+    files["acceptance_lsh"] = dict(bits=64, m=m, codes=codes, queries=qs,
+                                   **knn_case(R, codes, 64, m, qs, [1, 10, 100]))
+
+    # BASELINE config 1: n=1e6 uniform 64-bit (seed 1), 1000 queries (seed 2), m=4, k=10.
+    codes = R.gen_uniform(1000000, 64, 1)
+    qs = R.gen_uniform(1000, 64, 2)
+    files["config1"] = dict(bits=64, m=4, n=1000000, db_seed=1, q_seed=2, queries=qs,
+                            codes_sha256=digest(codes), **knn_case(R, codes, 64, 4, qs, [10]))
+
+    # index_test.cpp:96-112 RangeMatchesScanRandomized (range_search, next row §8f(1))
+    for bits in (32, 96, 100):
+        codes = R.gen_uniform(1500, bits, 8000 + bits)
+        qs = R.gen_uniform(12, bits, 9000 + bits)
+        d = dict(bits=bits, codes=codes, queries=qs)
+        for m in (2, 4, 5):
+            if (bits + m - 1) // m > 32:
+                continue
+            h = R.build(codes, bits, m)
+            for r in (0, 1, 5, bits // 3):
+                allids, alld, offs, trs = [], [], [0], []
+                for qi in range(qs.shape[0]):
+                    ids, dists, tr = h.range(qs[qi], r)
+                    allids.append(ids)
+                    alld.append(dists)
+                    offs.append(offs[-1] + ids.size)
+                    trs.append(tr)
+                d[f"m{m}_r{r}_ids"] = np.concatenate(allids).astype(np.uint32)
+                d[f"m{m}_r{r}_dists"] = np.concatenate(alld).astype(np.uint32)
+                d[f"m{m}_r{r}_offs"] = np.array(offs, np.uint64)
+                d[f"m{m}_r{r}_trace"] = np.stack(trs)
+        files[f"range_b{bits}"] = d
+
+    # table_test.cpp:34-43 / :65-104 semantics through MihIndex tables: bucket contents (ids in
+    # insertion order) for sampled buckets of a 2e4 x 64-bit, m=3 (22/21/21) index.
+    codes = R.gen_uniform(20000, 64, 777)
+    h = R.build(codes, 64, 3)
+    rng = np.random.default_rng(5)
+    recs_j, recs_v, recs_ids, recs_off = [], [], [], [0]
+    for j, s in enumerate((22, 21, 21)):
+        occupied = [(int(codes[i, 0]) >> (0 if j == 0 else 22 + 21 * (j - 1))) & ((1 << s) - 1)
+                    for i in rng.integers(0, 20000, 40)]
+        for v in occupied + [int(x) for x in rng.integers(0, 1 << s, 20)]:
+            ids = h.bucket(j, v)
+            recs_j.append(j)
+            recs_v.append(v)
+            recs_ids.append(ids)
+            recs_off.append(recs_off[-1] + ids.size)
+    files["buckets_m3"] = dict(bits=64, m=3, db_seed=777, n=20000,
+                               table=np.array(recs_j, np.uint32), value=np.array(recs_v, np.uint64),
+                               ids=np.concatenate(recs_ids).astype(np.uint32),
+                               offs=np.array(recs_off, np.uint64))
+
+    # gen_uniform pins (io.hpp:266-277): several widths and seeds.
+    pins = {}
+    for n, bits, seed in ((5, 64, 1), (7, 70, 181), (3, 256, 42), (4, 24, 501), (2, 130, 9)):
+        pins[f"gen_{n}_{bits}_{seed}"] = R.gen_uniform(n, bits, seed)
+    files["gen_uniform_pins"] = pins
+
+    for name, d in files.items():
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **{k: np.asarray(v) for k, v in d.items()})
+        print(f"{path}: {os.path.getsize(path)} bytes")
+
+
+if __name__ == "__main__":
+    main()

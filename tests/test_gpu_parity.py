@@ -1,0 +1,191 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden vectors and the
+C oracle. Integer work, so the bar is bit-exact: ids, distances and SearchTrace counters."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _mg():
+    import paper_1307_2982_b200 as mg
+
+    return mg
+
+
+def _trace_array(tr):
+    return np.array([[t.lookups, t.candidates, t.unique_candidates, t.distance_evaluations,
+                      t.final_radius] for t in tr], np.uint64)
+
+
+def _index(d, layout="auto"):
+    mg = _mg()
+    bits, m = int(d["bits"]), int(d["m"])
+    db = mg.CodeDatabase(bits, d["codes"])
+    if "lengths" in d:
+        ln, ps = d["lengths"], d["positions"]
+        subs, at = [], 0
+        for L in ln:
+            subs.append(list(ps[at:at + int(L)]))
+            at += int(L)
+        part = mg.Partition(bits, subs)
+    else:
+        part = mg.consecutive_partition(bits, m)
+    return mg.MihIndex.build(db, part, layout=layout)
+
+
+CASES = ["hand_worked", "knn_wide24", "duplicates", "self_queries", "nondivisible100",
+         "scratch_reuse32", "lsh_io_test", "interleaved64", "acceptance_lsh"]
+
+
+@pytest.mark.parametrize("layout", ["auto", "sparse"])
+@pytest.mark.parametrize("name", CASES)
+def test_knn_matches_reference_golden(cuda_ok, golden, name, layout):
+    d = golden(name)
+    if layout == "sparse" and min(int(d["bits"]) // int(d["m"]), 32) < 6:
+        pytest.skip("sparse directory needs s >= 6")
+    idx = _index(d, layout)
+    for key in sorted(k for k in d if k.startswith("ids_k")):
+        k = int(key.split("_k")[1])
+        ids, dists, tr = idx.knn_search_batch(d["queries"], k, with_trace=True)
+        assert np.array_equal(dists, d[f"dists_k{k}"]), (name, k)
+        assert np.array_equal(ids, d[f"ids_k{k}"]), (name, k)
+        assert np.array_equal(_trace_array(tr), d[f"trace_k{k}"]), (name, k)
+
+
+@pytest.mark.parametrize("bits", [64, 70])
+def test_knn_random_matches_reference(cuda_ok, golden, bits):
+    # index_test.cpp:127-154: k up to n drives the radius to the full width
+    mg = _mg()
+    d = golden(f"knn_random_b{bits}")
+    db = mg.gen_uniform(1200, bits, int(d["db_seed"]))
+    assert np.array_equal(db.raw_words(), d["codes"])
+    for m in (4, 6, 7):
+        idx = mg.MihIndex.build(db, mg.consecutive_partition(bits, m))
+        for k in (1, 2, 10, 100, 1200):
+            ids, dists, tr = idx.knn_search_batch(d["queries"], k, with_trace=True)
+            assert np.array_equal(ids, d[f"m{m}_ids_k{k}"]), (m, k)
+            assert np.array_equal(dists, d[f"m{m}_dists_k{k}"]), (m, k)
+            assert np.array_equal(_trace_array(tr), d[f"m{m}_trace_k{k}"]), (m, k)
+            si, sd = idx.scan_knn_batch(d["queries"], k)
+            assert np.array_equal(si, d[f"m{m}_ids_k{k}"]) and np.array_equal(sd, d[f"m{m}_dists_k{k}"])
+
+
+def test_acceptance_uniform(cuda_ok, golden):
+    # acceptance.cpp:134-172 criterion 2 (uniform lane), ids AND distances
+    mg = _mg()
+    d = golden("acceptance_uniform")
+    db = mg.gen_uniform(int(d["n"]), 64, int(d["db_seed"]))
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(64, int(d["m"])))
+    for k in (1, 10, 100):
+        ids, dists, tr = idx.knn_search_batch(d["queries"], k, with_trace=True)
+        assert np.array_equal(ids, d[f"ids_k{k}"]) and np.array_equal(dists, d[f"dists_k{k}"])
+        assert np.array_equal(_trace_array(tr), d[f"trace_k{k}"])
+        si, sd = idx.scan_knn_batch(d["queries"], k)
+        assert np.array_equal(si, d[f"ids_k{k}"]) and np.array_equal(sd, d[f"dists_k{k}"])
+
+
+@pytest.mark.parametrize("layout", ["auto", "sparse"])
+def test_config1_golden(cuda_ok, golden, layout):
+    # BASELINE config 1: n=1e6 uniform 64-bit, 1000 queries, m=4, k=10
+    mg = _mg()
+    d = golden("config1")
+    db = mg.gen_uniform(int(d["n"]), 64, int(d["db_seed"]))
+    qs = mg.gen_uniform(1000, 64, int(d["q_seed"])).raw_words()
+    assert np.array_equal(qs, d["queries"])
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(64, 4), layout=layout)
+    ids, dists, tr = idx.knn_search_batch(qs, 10, with_trace=True)
+    assert np.array_equal(ids, d["ids_k10"]) and np.array_equal(dists, d["dists_k10"])
+    assert np.array_equal(_trace_array(tr), d["trace_k10"])
+    si, sd = idx.scan_knn_batch(qs, 10)
+    assert np.array_equal(si, d["ids_k10"]) and np.array_equal(sd, d["dists_k10"])
+
+
+@pytest.mark.parametrize("layout", ["auto", "sparse"])
+def test_bucket_contents_match_reference(cuda_ok, golden, layout):
+    # table_test.cpp:34-43 (insertion order within a bucket), :65-104 (map equivalence)
+    mg = _mg()
+    d = golden("buckets_m3")
+    db = mg.gen_uniform(int(d["n"]), 64, int(d["db_seed"]))
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(64, 3), layout=layout)
+    offs = d["offs"]
+    for i in range(d["table"].size):
+        got = idx.table(int(d["table"][i])).bucket_lookup(int(d["value"][i]))
+        assert np.array_equal(got, d["ids"][int(offs[i]):int(offs[i + 1])])
+
+
+def test_single_query_api_and_trace(cuda_ok, golden):
+    # index_test.cpp:73-94 HandWorkedKnn through the single-query facade
+    mg = _mg()
+    db = mg.CodeDatabase(6)
+    for w in (0b000000, 0b000001, 0b111111):
+        db.append_words(np.array([w], np.uint64))
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(6, 2))
+    tr = mg.SearchTrace()
+    res = idx.knn_search(mg.BinaryCode(np.array([0], np.uint64), 6), 2, tr)
+    assert res == [mg.Neighbor(0, 0), mg.Neighbor(1, 1)]
+    assert (tr.final_radius, tr.lookups, tr.candidates, tr.unique_candidates) == (1, 2, 3, 2)
+
+
+def test_error_contract(cuda_ok):
+    # index_test.cpp:250-268 ValidationAndEdges
+    mg = _mg()
+    db = mg.gen_uniform(10, 64, 1)
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(64, 2))
+    q = mg.BinaryCode(np.array([5], np.uint64), 64)
+    with pytest.raises(ValueError):
+        idx.knn_search(q, 11)
+    with pytest.raises(ValueError):
+        idx.knn_search(mg.BinaryCode(np.array([0], np.uint64), 32), 1)
+    assert idx.knn_search(q, 0) == []
+    ids, dists, tr = idx.knn_search_batch(np.zeros((3, 1), np.uint64), 0, with_trace=True)
+    assert ids.shape == (3, 0) and not _trace_array(tr).any()
+    empty = mg.MihIndex.build(mg.CodeDatabase(64), mg.consecutive_partition(64, 2))
+    assert empty.knn_search(q, 0) == []
+    with pytest.raises(ValueError):
+        empty.knn_search(q, 1)
+
+
+def test_free_scan_knn(cuda_ok, golden):
+    mg = _mg()
+    d = golden("knn_random_b70")
+    db = mg.CodeDatabase(70, d["codes"])
+    q = mg.BinaryCode(d["queries"][3], 70)
+    res = mg.scan_knn(db, q, 100)
+    assert [r.id for r in res] == list(d["m4_ids_k100"][3])
+    assert [r.dist for r in res] == list(d["m4_dists_k100"][3])
+
+
+def test_heavy_ties_and_buffer_overflow(cuda_ok, port):
+    # 40k copies of a handful of codes: ties at d_k far beyond the per-query buffer, exercising
+    # the re-run and large-selection paths (scan.hpp:42 tie rule).
+    mg = _mg()
+    rng = np.random.default_rng(7)
+    base = rng.integers(0, 2**63, size=5, dtype=np.uint64)
+    codes = base[rng.integers(0, 5, size=40000)] ^ (np.uint64(1) << rng.integers(0, 3, 40000).astype(np.uint64))
+    codes = codes.reshape(-1, 1)
+    qs = np.concatenate([base.reshape(-1, 1), rng.integers(0, 2**63, size=(3, 1), dtype=np.uint64)])
+    idx = mg.MihIndex.build(mg.CodeDatabase(64, codes), mg.consecutive_partition(64, 4))
+    h = port.build(codes, 64, 4)
+    for k in (1, 50, 9000, 20000):
+        ids, dists, tr = idx.knn_search_batch(qs, k, with_trace=True)
+        oi, od, ot = h.knn(qs, k)
+        assert np.array_equal(dists, od), k
+        assert np.array_equal(ids, oi), k
+        assert np.array_equal(_trace_array(tr), ot), k
+        si, sd = idx.scan_knn_batch(qs, k)
+        assert np.array_equal(si, oi) and np.array_equal(sd, od), k
+
+
+@pytest.mark.parametrize("bits,m,n", [(128, 6, 200000), (256, 8, 100000), (64, 3, 300000), (64, 2, 200000)])
+def test_random_shapes_vs_oracle(cuda_ok, port, bits, m, n):
+    mg = _mg()
+    db = mg.gen_uniform(n, bits, 1000 + bits + m)
+    qs = mg.gen_uniform(40, bits, 2000 + bits + m).raw_words()
+    for layout in ("auto", "sparse"):
+        idx = mg.MihIndex.build(db, mg.consecutive_partition(bits, m), layout=layout)
+        h = port.build(db.raw_words(), bits, m)
+        for k in (1, 25, 100):
+            ids, dists, tr = idx.knn_search_batch(qs, k, with_trace=True)
+            oi, od, ot = h.knn(qs, k)
+            assert np.array_equal(ids, oi) and np.array_equal(dists, od), (layout, k)
+            assert np.array_equal(_trace_array(tr), ot), (layout, k)

@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""Exact Hamming kNN throughput on B200 (BASELINE.json metric: exact kNN queries/s, n=1B, k=100).
+
+Default workload = BASELINE config 4: n = 1e9 64-bit Gaussian-mixture sign-projection codes,
+10k queries from the same generator, k = 100, m = 2 sparse tables of 32-bit substrings, id-range
+sharded over the ranks (one process per GPU, NCCL all-gather + exact k-way merge for N > 1).
+
+One step = one pass of the MIH kNN hot path over the whole 10k-query batch.
+  value : queries/s with queries and results resident in HBM (device-pointer C ABI call),
+          whole job (all ranks), timed with CUDA events, max over ranks.
+  e2e   : the same through the host-pointer C ABI (mihg_knn_batch): pinned host queries in,
+          host results out, copies inside the timed region.
+  roofline : the MIH probe kernel's algorithmic bytes (8*lookups + 4*candidates
+          + (b/8)*unique, from the reference-identical SearchTrace counters) over its CUDA-event
+          time, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline : the reference's own MihIndex::knn_search (oracle/_ref, built from the reference
+          headers) on the host cores, on a bounded sample of this workload's queries.
+
+`--impl reference` times only that CPU reference arm (rank 0; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(n=1_000_000, bits=64, m=4, k=10, nq=1000, data="uniform", db_seed=1, q_seed=2),
+    2: dict(n=10_000_000, bits=128, m=6, k=10, nq=10000, data="mixture", model_seed=0x2C0FFEE,
+            db_seed=0x2D0001, q_seed=0x2D0002),
+    3: dict(n=100_000_000, bits=64, m=3, k=100, nq=10000, data="uniform", db_seed=3, q_seed=4),
+    4: dict(n=1_000_000_000, bits=64, m=2, k=100, nq=10000, data="mixture", model_seed=0x4C0FFEE,
+            db_seed=0x4D0001, q_seed=0x4D0002),
+    5: dict(n=1_000_000_000, bits=256, m=8, k=100, nq=10000, data="uniform", db_seed=5, q_seed=6),
+}
+MIX_DIM, MIX_COMPS = 128, 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override database size (testing only)")
+    ap.add_argument("--nq", type=int, default=0)
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="queries per CPU-reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+    if args.nq:
+        cfg["nq"] = args.nq
+    if args.k:
+        cfg["k"] = args.k
+    return cfg
+
+
+def wpc(bits):
+    return (bits + 63) // 64
+
+
+def shard_range(n, rank, world):
+    per = (n + world - 1) // world
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sms, mx, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                sms.append(float(r[1]))
+                mx = float(r[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------------------------
+def make_codes_device(cfg, lo, hi, seed, torch, dev, lib):
+    """Codes [lo, hi) of the workload's generator, resident on `dev` as int64 words."""
+    W = wpc(cfg["bits"])
+    n = hi - lo
+    out = torch.empty((max(n, 1), W), dtype=torch.int64, device=dev)
+    if cfg["data"] == "mixture":
+        from paper_1307_2982_b200 import _lib
+        _lib.check(lib.mihg_gen_mixture_device(lo, n, cfg["bits"], MIX_DIM, MIX_COMPS, cfg["model_seed"],
+                                               seed, C.c_void_p(out.data_ptr()), None))
+        torch.cuda.synchronize(dev)
+    else:
+        host = np.zeros((max(n, 1), W), np.uint64)
+        from paper_1307_2982_b200 import _lib
+        _lib.check(lib.mihg_gen_uniform_range(lo, n, cfg["bits"], seed, host.ctypes.data_as(_lib.u64p)))
+        out.copy_(torch.from_numpy(host.view(np.int64)))
+    return out
+
+
+def make_codes_host_cpu(cfg, lo, hi, seed):
+    """The same codes generated on the host only (CPU reference arm: no GPU code involved)."""
+    import oracle
+
+    if cfg["data"] == "mixture":
+        return oracle.port().gen_mixture(lo, hi - lo, cfg["bits"], MIX_DIM, MIX_COMPS, cfg["model_seed"], seed)
+    R = oracle.ref()
+    if lo == 0:
+        return R.gen_uniform(hi, cfg["bits"], seed)
+    return R.gen_uniform(hi, cfg["bits"], seed)[lo:]
+
+
+def config_desc(cfg, args, world):
+    d = {"workload": f"BASELINE config {args.config}: exact {cfg['k']}-NN over n={cfg['n']:.0e} "
+                     f"{cfg['bits']}-bit {cfg['data']} codes, {cfg['nq']} queries, MIH m={cfg['m']}",
+         "n": cfg["n"], "bits": cfg["bits"], "m": cfg["m"], "k": cfg["k"], "queries": cfg["nq"],
+         "data_generator": cfg["data"], "parallelism": f"id-range shards x{world}",
+         "l2_policy": "inputs larger than L2 (index >> 126 MB); no flush"}
+    if cfg["data"] == "mixture":
+        d.update({"mixture": {"dim": MIX_DIM, "components": MIX_COMPS, "sigma_rel": 1.0,
+                              "model_seed": cfg["model_seed"], "db_seed": cfg["db_seed"],
+                              "q_seed": cfg["q_seed"], "arith": "exact int8 (csrc/gen.cu)"}})
+    else:
+        d.update({"db_seed": cfg["db_seed"], "q_seed": cfg["q_seed"], "generator": "gen_uniform (mt19937_64)"})
+    return d
+
+
+# ---------------------------------------------------------------------------------------------
+def cpu_reference_run(cfg, codes_host, queries_host, steps, warmup, sample):
+    """Reference MihIndex::knn_search (oracle/_ref) with all host threads, `sample` queries per
+    step. Returns (q/s, threads, build_seconds, per-step seconds)."""
+    import oracle
+
+    R = oracle.ref()
+    threads = os.cpu_count() or 1
+    t0 = time.time()
+    h = R.build_parallel(codes_host, cfg["bits"], cfg["m"])
+    build_s = time.time() - t0
+    nq = queries_host.shape[0]
+    times = []
+    for s in range(warmup + steps):
+        lo = (s * sample) % max(1, nq - sample + 1)
+        q = queries_host[lo:lo + sample]
+        t = time.perf_counter()
+        h.knn(q, cfg["k"], threads=threads)
+        dt = time.perf_counter() - t
+        if s >= warmup:
+            times.append(dt)
+    del h
+    qps = sample * len(times) / sum(times)
+    return qps, threads, build_s, times
+
+
+def run_reference_arm(args):
+    cfg = workload(args)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import oracle
+
+    if not oracle.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmihref.so not built"}))
+        return
+    sample = args.cpu_sample or 64
+    t0 = time.time()
+    codes = make_codes_host_cpu(cfg, 0, cfg["n"], cfg["db_seed"])
+    queries = make_codes_host_cpu(cfg, 0, cfg["nq"], cfg["q_seed"])
+    gen_s = time.time() - t0
+    qps, threads, build_s, times = cpu_reference_run(cfg, codes, queries, args.steps, args.warmup, sample)
+    line = {
+        "metric": "exact kNN queries/s", "value": qps, "unit": "queries/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": config_desc(cfg, args, 1),
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample} queries per step of the {cfg['nq']}-query batch, full "
+                                   f"n={cfg['n']} reference index (MihIndex::knn_search, "
+                                   f"one SearchScratch per thread); index build {build_s:.0f}s, "
+                                   f"data gen {gen_s:.0f}s excluded"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+
+    from paper_1307_2982_b200 import _lib
+    import paper_1307_2982_b200 as mg
+
+    cfg = workload(args)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.lib()
+    bits, m, k, nq, W = cfg["bits"], cfg["m"], cfg["k"], cfg["nq"], wpc(cfg["bits"])
+    lo, hi = shard_range(cfg["n"], rank, world)
+
+    # ---- data + index (setup, untimed) ----
+    t0 = time.time()
+    codes = make_codes_device(cfg, lo, hi, cfg["db_seed"], torch, dev, L)
+    queries = make_codes_device(cfg, 0, nq, cfg["q_seed"], torch, dev, L)
+    gen_s = time.time() - t0
+    t0 = time.time()
+    idx = mg.MihIndex.build_from_device(codes.data_ptr(), hi - lo, bits, mg.consecutive_partition(bits, m),
+                                        local_rank, id_base=lo)
+    torch.cuda.synchronize(dev)
+    build_s = time.time() - t0
+    del codes  # the index holds its own copy
+    torch.cuda.empty_cache()
+
+    kk = min(k, hi - lo)  # shard-local k (exact: global top-k is inside the union of local top-k)
+    ids = torch.empty((nq, kk), dtype=torch.int32, device=dev)
+    dists = torch.empty((nq, kk), dtype=torch.int32, device=dev)
+    if world > 1:
+        all_ids = torch.empty((world, nq, kk), dtype=torch.int32, device=dev)
+        all_d = torch.empty((world, nq, kk), dtype=torch.int32, device=dev)
+        out_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        out_d = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
+                              stream=stream.cuda_stream)
+        if world > 1:
+            dist.all_gather_into_tensor(all_ids, ids)
+            dist.all_gather_into_tensor(all_d, dists)
+            _lib.check(L.mihg_merge_topk_device(C.c_void_p(all_ids.data_ptr()), C.c_void_p(all_d.data_ptr()),
+                                                world, nq, kk, k, C.c_void_p(out_ids.data_ptr()),
+                                                C.c_void_p(out_d.data_ptr()), C.c_void_p(stream.cuda_stream)))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: device-resident inputs ----
+    prof0 = _lib.Profile()
+    L.mihg_profile_reset()
+    L.mihg_profile_enable(1)
+    L.mihg_profile_read(C.byref(prof0))
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    prof1 = _lib.Profile()
+    L.mihg_profile_read(C.byref(prof1))
+    L.mihg_profile_enable(0)
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = nq * args.steps / (ms / 1000.0)
+    launches = int(prof1.kernel_launches - prof0.kernel_launches)
+    probe_ms = prof1.probe_ms / args.steps
+    probe_launches = prof1.probe_launches / args.steps
+
+    # ---- algorithmic bytes from the reference-identical traces (untimed run) ----
+    tr = torch.empty((nq, 5), dtype=torch.int64, device=dev)
+    idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(), tr.data_ptr(),
+                          stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    t = tr.cpu().numpy()
+    lookups, cands, uniq, radius = (t[:, 0].astype(np.float64), t[:, 1].astype(np.float64),
+                                    t[:, 2].astype(np.float64), t[:, 4].astype(np.float64))
+    alg_bytes = float((8 * lookups + 4 * cands + (bits / 8) * uniq).sum())
+    popc64 = float(uniq.sum() * W)
+
+    # ---- e2e through the host-pointer C ABI ----
+    hq = torch.from_numpy(np.ascontiguousarray(queries.cpu().numpy())).pin_memory()
+    hid = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    hd = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    if world == 1:
+        def e2e_step():
+            _lib.check(L.mihg_knn_batch(idx._h, C.cast(C.c_void_p(hq.data_ptr()), _lib.u64p), nq, k,
+                                        C.cast(C.c_void_p(hid.data_ptr()), _lib.u32p),
+                                        C.cast(C.c_void_p(hd.data_ptr()), _lib.u32p), None))
+    else:
+        dq = torch.empty_like(queries)
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            idx.knn_search_device(dq.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
+                                  stream=stream.cuda_stream)
+            dist.all_gather_into_tensor(all_ids, ids)
+            dist.all_gather_into_tensor(all_d, dists)
+            _lib.check(L.mihg_merge_topk_device(C.c_void_p(all_ids.data_ptr()), C.c_void_p(all_d.data_ptr()),
+                                                world, nq, kk, k, C.c_void_p(out_ids.data_ptr()),
+                                                C.c_void_p(out_d.data_ptr()), C.c_void_p(stream.cuda_stream)))
+            hid.copy_(out_ids, non_blocking=True)
+            hd.copy_(out_d, non_blocking=True)
+            torch.cuda.synchronize(dev)
+
+    e2e_step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = nq * args.steps / (e2e_ms / 1000.0)
+
+    # ---- roofline ----
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if peak else None, "traffic": None,
+                "kernel": "mih_probe_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+                "alg_bytes_per_step": alg_bytes, "probe_ms_per_step": probe_ms,
+                "probe_launches_per_step": probe_launches,
+                "step_frac_of_roofline": (alg_bytes / (ms_per_step / 1000.0) / 1e9) / peak,
+                "popc64_per_step": popc64,
+                "mean_trace": {"lookups": float(lookups.mean()), "candidates": float(cands.mean()),
+                               "unique": float(uniq.mean()), "final_radius": float(radius.mean())}}
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+
+            if oracle.have_ref():
+                sample = args.cpu_sample or 64
+                db_host = make_codes_device(cfg, 0, cfg["n"], cfg["db_seed"], torch, dev, L).cpu().numpy().view(np.uint64)
+                torch.cuda.empty_cache()
+                qh = queries.cpu().numpy().view(np.uint64)
+                qps, threads, build_cpu_s, _ = cpu_reference_run(cfg, db_host, qh, 2, 1, sample)
+                del db_host
+                cpu = {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                       "sample": f"{sample} queries per step x 2 steps, full n={cfg['n']} reference "
+                                 f"index (oracle/_ref, MihIndex::knn_search, {threads} threads); "
+                                 f"reference index build {build_cpu_s:.0f}s excluded"}
+            else:
+                cpu = {"value": None, "unavailable": "oracle/_ref not built"}
+        except Exception as e:  # the baseline must not sink the GPU measurement
+            cpu = {"value": None, "error": repr(e)[:300]}
+
+    if rank == 0:
+        line = {
+            "metric": "exact kNN queries/s", "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": config_desc(cfg, args, world),
+            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(nq * W * 8),
+                    "d2h_bytes_per_step": int(nq * k * 8)},
+            "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "setup": {"gen_s": gen_s, "index_build_s": build_s, "index_device_bytes": idx.device_bytes()},
+        }
+        print(json.dumps(line))
+    idx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,28 @@ int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint3
 
 /* gen_uniform(n, bits, seed) — io.hpp:266-277 (std::mt19937_64, standard-specified). Host. */
 int mihg_gen_uniform(uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out);
+/* Codes [first, first + n) of gen_uniform(., bits, seed) — an id-range shard of the same stream. */
+int mihg_gen_uniform_range(uint64_t first, uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out);
+
+/* Live profiling: kernel launch count of this library (process-wide), and CUDA-event time of the
+ * MIH probe kernel launches (recorded on their own stream) while enabled. */
+typedef struct mihg_profile {
+  uint64_t kernel_launches;
+  double probe_ms;
+  uint64_t probe_launches;
+  double scan_ms;
+  uint64_t scan_launches;
+} mihg_profile;
+int mihg_profile_enable(int on);
+void mihg_profile_reset(void);
+int mihg_profile_read(mihg_profile* out);
+
+/* Seeded Gaussian-mixture sign-projection codes (BASELINE configs 2 and 4; not in the reference,
+ * which has gen_correlated_vectors + lsh_encode, io.hpp:245-262, :312-331). Exact integer
+ * arithmetic, defined in paper_1307_2982_b200/csrc/gen.cu. Writes codes [first, first + n) as
+ * n * ceil(bits/64) words to device memory. bits <= 256, dim % 4 == 0 and dim <= 256, comps <= 256. */
+int mihg_gen_mixture_device(uint64_t first, uint64_t n, uint32_t bits, uint32_t dim, uint32_t comps,
+                            uint64_t model_seed, uint64_t data_seed, uint64_t* d_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,14 @@ class Port(_Lib):
         self.lib.or_scan_knn.argtypes = [_u64p, C.c_uint64, C.c_uint32, _u64p, C.c_uint64,
                                          C.c_uint32, _u32p, _u32p]
         self.lib.or_gen_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, _u64p]
+        self.lib.or_gen_mixture.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
+                                            C.c_uint32, C.c_uint64, C.c_uint64, _u64p, C.c_int]
+
+    def gen_mixture(self, first, n, bits, dim, comps, model_seed, data_seed, threads=None):
+        out = np.zeros(max(n * wpc(bits), 1), np.uint64)
+        self._check(self.lib.or_gen_mixture(first, n, bits, dim, comps, model_seed, data_seed,
+                                            _p64(out), threads or os.cpu_count() or 1))
+        return out[: n * wpc(bits)].reshape(n, wpc(bits))
 
     def gen_uniform(self, n, bits, seed):
         out = np.zeros(max(n * wpc(bits), 1), np.uint64)
@@ -124,6 +132,8 @@ class Ref(_Lib):
         L.ref_index_build.argtypes = [_u64p, C.c_uint64, C.c_uint32, C.c_uint32, _u32p, _u32p,
                                       C.POINTER(C.c_void_p)]
         L.ref_index_free.argtypes = [C.c_void_p]
+        L.ref_index_build_parallel.argtypes = [_u64p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                               C.POINTER(C.c_void_p)]
         L.ref_knn.argtypes = [C.c_void_p, _u64p, C.c_uint64, C.c_uint32, _u32p, _u32p, _u64p, C.c_int]
         L.ref_range.argtypes = [C.c_void_p, _u64p, C.c_uint32, _u32p, _u32p, C.c_uint64, _u64p, _u64p]
         L.ref_bucket.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, _u32p, C.c_uint64, _u64p]
@@ -157,6 +167,14 @@ class Ref(_Lib):
         ln = None if lengths is None else np.ascontiguousarray(lengths, np.uint32)
         ps = None if positions is None else np.ascontiguousarray(positions, np.uint32)
         self._check(self.lib.ref_index_build(_p64(codes), n, bits, m, _p32(ln), _p32(ps), C.byref(h)))
+        return _Handle(self, h, bits, n)
+
+    def build_parallel(self, codes, bits, m):
+        """Tables built concurrently through SubstringTable::build + MihIndex::assemble."""
+        codes = np.ascontiguousarray(codes, np.uint64).reshape(-1)
+        n = codes.size // wpc(bits)
+        h = C.c_void_p()
+        self._check(self.lib.ref_index_build_parallel(_p64(codes), n, bits, m, C.byref(h)))
         return _Handle(self, h, bits, n)
 
     def scan_knn(self, codes, bits, queries, k, threads=None):

@@ -14,6 +14,7 @@
  */
 #include "mih_oracle.h"
 
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -512,5 +513,83 @@ int or_scan_knn(const uint64_t* codes, uint64_t n, uint32_t bits, const uint64_t
   free(hist);
   free(dd);
   free(fill);
+  return 0;
+}
+
+/* ---- Gaussian-mixture sign-projection generator: C restatement of
+ * paper_1307_2982_b200/csrc/gen.cu (exact integer arithmetic; see the definition there). Used to
+ * pin the GPU generator and to give the CPU reference arm its inputs without the GPU. */
+static uint64_t sm64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+static int g5(uint64_t u) {
+  return (int)(u & 31) + (int)((u >> 5) & 31) + (int)((u >> 10) & 31) + (int)((u >> 15) & 31) - 62;
+}
+static int g6(uint64_t u) {
+  return (int)(u & 63) + (int)((u >> 6) & 63) + (int)((u >> 12) & 63) + (int)((u >> 18) & 63) - 126;
+}
+
+typedef struct {
+  uint64_t first, lo, hi;
+  uint32_t bits, dim, comps;
+  const int32_t* Wt; /* [dim][bits]: transposed so the inner loop runs over output bits */
+  const int8_t* mu;
+  uint64_t hC, hX;
+  uint64_t* out;
+} mix_job;
+
+static void* mix_worker(void* arg) {
+  const mix_job* j = (const mix_job*)arg;
+  const uint32_t per = (j->dim + 2) / 3, wpc = (j->bits + 63) / 64, bits = j->bits;
+  int32_t acc[256];
+  for (uint64_t r = j->lo; r < j->hi; ++r) {
+    const uint64_t i = j->first + r;
+    const uint32_t c = (uint32_t)(sm64(j->hC ^ i) % j->comps);
+    uint64_t u = 0;
+    for (uint32_t b = 0; b < bits; ++b) acc[b] = 0;
+    for (uint32_t d = 0; d < j->dim; ++d) {
+      if (d % 3 == 0) u = sm64(j->hX ^ (i * per + d / 3));
+      const int32_t xd = j->mu[(size_t)c * j->dim + d] + g5(u >> (20 * (d % 3)));
+      const int32_t* wc = j->Wt + (size_t)d * bits;
+      for (uint32_t b = 0; b < bits; ++b) acc[b] += wc[b] * xd;
+    }
+    for (uint32_t w = 0; w < wpc; ++w) j->out[r * wpc + w] = 0;
+    for (uint32_t b = 0; b < bits; ++b)
+      if (acc[b] >= 0) j->out[r * wpc + b / 64] |= 1ULL << (b % 64);
+  }
+  return NULL;
+}
+
+int or_gen_mixture(uint64_t first, uint64_t n, uint32_t bits, uint32_t dim, uint32_t comps,
+                   uint64_t model_seed, uint64_t data_seed, uint64_t* out, int nthreads) {
+  if (bits == 0 || bits > 256 || dim == 0 || dim % 4 || dim > 256 || comps == 0 || comps > 256)
+    return fail(1, "gen_mixture: bad shape");
+  int32_t* W = (int32_t*)malloc(sizeof(int32_t) * bits * dim);
+  int8_t* mu = (int8_t*)malloc((size_t)comps * dim);
+  const uint64_t hW = sm64(model_seed ^ (1ULL * 0xD6E8FEB86659FD93ULL));
+  const uint64_t hMu = sm64(model_seed ^ (2ULL * 0xD6E8FEB86659FD93ULL));
+  /* W[j][d] = g6(h(model_seed, 1, j*dim + d)), stored transposed */
+  for (uint64_t t = 0; t < (uint64_t)bits * dim; ++t) W[(t % dim) * bits + t / dim] = g6(sm64(hW ^ t));
+  for (uint64_t t = 0; t < (uint64_t)comps * dim; ++t) mu[t] = (int8_t)g5(sm64(hMu ^ t));
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  mix_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    mix_job* j = &jobs[t];
+    j->first = first;
+    j->lo = n * (uint64_t)t / (uint64_t)nthreads;
+    j->hi = n * (uint64_t)(t + 1) / (uint64_t)nthreads;
+    j->bits = bits, j->dim = dim, j->comps = comps, j->Wt = W, j->mu = mu, j->out = out;
+    j->hC = sm64(data_seed ^ (3ULL * 0xD6E8FEB86659FD93ULL));
+    j->hX = sm64(data_seed ^ (4ULL * 0xD6E8FEB86659FD93ULL));
+    pthread_create(&th[t], NULL, mix_worker, j);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(W);
+  free(mu);
   return 0;
 }

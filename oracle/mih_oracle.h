@@ -27,6 +27,9 @@ int or_range(const or_index* idx, const uint64_t* q, uint32_t r, uint32_t* ids, 
 int or_scan_knn(const uint64_t* codes, uint64_t n, uint32_t bits, const uint64_t* queries,
                 uint64_t nq, uint32_t k, uint32_t* ids, uint32_t* dists);
 
+int or_gen_mixture(uint64_t first, uint64_t n, uint32_t bits, uint32_t dim, uint32_t comps,
+                   uint64_t model_seed, uint64_t data_seed, uint64_t* out, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -133,6 +133,37 @@ int ref_index_build(const uint64_t* codes, uint64_t n, uint32_t bits, uint32_t m
   });
 }
 
+// Same index as ref_index_build, with the m tables built concurrently (one thread per table)
+// through the reference's public SubstringTable::build (table.hpp:91-159) and
+// MihIndex::assemble (index.hpp:124-141); pairs are formed exactly as MihIndex::build does
+// (index.hpp:113-117), so every table is identical. Only the wall time of the setup differs.
+int ref_index_build_parallel(const uint64_t* codes, uint64_t n, uint32_t bits, uint32_t m,
+                             void** out) {
+  return guarded([&] {
+    mih::CodeDatabase db = make_db(codes, n, bits);
+    mih::Partition part = mih::consecutive_partition(bits, m);
+    std::vector<mih::SubstringTable> tables(m);
+    std::vector<std::exception_ptr> errs(m);
+    std::vector<std::thread> pool;
+    for (uint32_t j = 0; j < m; ++j)
+      pool.emplace_back([&, j] {
+        try {
+          std::vector<std::pair<uint64_t, uint32_t>> pairs;
+          pairs.reserve(n);
+          for (uint64_t i = 0; i < n; ++i)
+            pairs.emplace_back(mih::extract_substring(db.code(i), part, j), static_cast<uint32_t>(i));
+          tables[j] = mih::SubstringTable::build(part.length(j), std::move(pairs));
+        } catch (...) {
+          errs[j] = std::current_exception();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    *out = new mih::MihIndex(mih::MihIndex::assemble(std::move(db), std::move(part), std::move(tables)));
+  });
+}
+
 void ref_index_free(void* h) { delete static_cast<mih::MihIndex*>(h); }
 
 int ref_index_table_s(void* h, uint32_t j, uint32_t* s) {

@@ -52,6 +52,12 @@ class TableInfo(C.Structure):
                 ("escaped_blocks", C.c_uint64)]
 
 
+class Profile(C.Structure):
+    _fields_ = [("kernel_launches", C.c_uint64), ("probe_ms", C.c_double),
+                ("probe_launches", C.c_uint64), ("scan_ms", C.c_double),
+                ("scan_launches", C.c_uint64)]
+
+
 # every symbol include/mihg.h declares: (name, restype, argtypes)
 SYMBOLS = [
     ("mihg_last_error", C.c_char_p, []),
@@ -79,6 +85,13 @@ SYMBOLS = [
                                          C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
     ("mihg_gen_uniform", C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, u64p]),
+    ("mihg_gen_uniform_range", C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, u64p]),
+    ("mihg_gen_mixture_device", C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p,
+                                          C.c_void_p]),
+    ("mihg_profile_enable", C.c_int, [C.c_int]),
+    ("mihg_profile_reset", None, []),
+    ("mihg_profile_read", C.c_int, [C.POINTER(Profile)]),
 ]
 
 _lib = None

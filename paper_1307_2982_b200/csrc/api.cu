@@ -83,6 +83,11 @@ struct Mt64 {
 
 }  // namespace
 
+namespace mihg {
+void set_last_error(const std::string& msg) { g_err = msg; }
+uint64_t launch_count();
+}  // namespace mihg
+
 extern "C" {
 
 const char* mihg_last_error(void) { return g_err.c_str(); }
@@ -303,12 +308,38 @@ int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint3
   });
 }
 
+int mihg_profile_enable(int on) {
+  mihg::profile().enabled = on != 0;
+  return MIHG_OK;
+}
+
+void mihg_profile_reset(void) {
+  mihg::ProfileState& p = mihg::profile();
+  p.probe_ms = p.scan_ms = 0;
+  p.probe_launches = p.scan_launches = 0;
+}
+
+int mihg_profile_read(mihg_profile* out) {
+  const mihg::ProfileState& p = mihg::profile();
+  out->kernel_launches = mihg::launch_count();
+  out->probe_ms = p.probe_ms;
+  out->probe_launches = p.probe_launches;
+  out->scan_ms = p.scan_ms;
+  out->scan_launches = p.scan_launches;
+  return MIHG_OK;
+}
+
 int mihg_gen_uniform(uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out) {
+  return mihg_gen_uniform_range(0, n, bits, seed, out);
+}
+
+int mihg_gen_uniform_range(uint64_t first, uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out) {
   return guarded([&] {
     if (bits == 0 || bits > mihg::kMaxCodeBits) throw mihg::InvalidArgument("gen_uniform: bad width");
     Mt64 rng(seed);
     const uint32_t wpc = mihg::words_per_code(bits);
     const uint64_t mask = (bits & 63) == 0 ? ~uint64_t(0) : ((uint64_t(1) << (bits & 63)) - 1);
+    for (uint64_t i = 0; i < first * wpc; ++i) rng();  // the stream is sequential: skip draws
     for (uint64_t i = 0; i < n; ++i) {
       uint64_t* w = out + i * wpc;
       for (uint32_t k = 0; k < wpc; ++k) w[k] = rng();

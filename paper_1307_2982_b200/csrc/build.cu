@@ -6,6 +6,7 @@
 //      sparse: one warp per 64-bucket directory block -> 3-bit-plane counts + entry base,
 //              escape records (65 exact starts) for blocks holding a bucket of >= 7 entries.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <string>
 
@@ -30,6 +31,14 @@ void upload_binomials() {
       tab[n][k] = k > n ? 0 : (k == 0 || k == n) ? 1 : tab[n - 1][k - 1] + tab[n - 1][k];
     }
   MIHG_CUDA(cudaMemcpyToSymbol(c_binom, tab, sizeof(tab)));
+}
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(); }
+ProfileState& profile() {
+  static ProfileState p;
+  return p;
 }
 
 bool sync_debug() {

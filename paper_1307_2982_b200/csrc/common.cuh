@@ -26,8 +26,10 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define MIHG_CUDA(x) ::mihg::cuda_check((x), #x, __FILE__, __LINE__)
 // MIHG_SYNC_DEBUG=1 in the environment: synchronize after every launch to localize faults.
 bool sync_debug();
+void count_launch();  // process-wide counter of this library's kernel launches (mihg_profile)
 #define MIHG_LAUNCH()                                                                     \
   do {                                                                                    \
+    ::mihg::count_launch();                                                               \
     ::mihg::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);          \
     if (::mihg::sync_debug())                                                             \
       ::mihg::cuda_check(cudaDeviceSynchronize(), "kernel execution", __FILE__, __LINE__); \
@@ -177,5 +179,16 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 inline uint32_t ceil_div_u32(uint64_t a, uint64_t b) { return uint32_t((a + b - 1) / b); }
 
 int device_sm_count();
+void set_last_error(const std::string& msg);
+
+// Live per-kernel timing (CUDA events on the launching stream), enabled by mihg_profile_enable.
+struct ProfileState {
+  bool enabled = false;
+  double probe_ms = 0;
+  uint64_t probe_launches = 0;
+  double scan_ms = 0;
+  uint64_t scan_launches = 0;
+};
+ProfileState& profile();  // thread-local message behind mihg_last_error()
 
 }  // namespace mihg

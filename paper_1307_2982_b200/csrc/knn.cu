@@ -40,8 +40,11 @@ struct Workspace {
   DeviceBuffer<uint64_t> lookups_prefix;
   uint32_t* h_counter = nullptr;
   cudaStream_t st = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~Workspace() {
     if (h_counter) cudaFreeHost(h_counter);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
   }
 };
 
@@ -429,6 +432,8 @@ void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
   ws->trc = DeviceBuffer<unsigned long long>(2 * nq, st);
   ws->lookups_prefix = DeviceBuffer<uint64_t>(b1 + 1, st);
   MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_counter), 16));
+  MIHG_CUDA(cudaEventCreate(&ws->ev0));
+  MIHG_CUDA(cudaEventCreate(&ws->ev1));
 }
 
 uint32_t read_counter(const uint32_t* d, uint32_t* h, cudaStream_t st) {
@@ -486,7 +491,10 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
       p.active = act_in;
       p.ring = ring;
       plan_round(p, nact);
+      ProfileState& prof = profile();
+      if (prof.enabled) MIHG_CUDA(cudaEventRecord(ws.ev0, st));
       dispatch_probe(p, d_tr != nullptr, st);
+      if (prof.enabled) MIHG_CUDA(cudaEventRecord(ws.ev1, st));
     }
     MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
     const unsigned g = unsigned((nact * 32 + 255) / 256);
@@ -494,7 +502,13 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
                                              ws.hist.get(), b1, ws.ubound.get(), k, r,
                                              ws.final_r.get(), ws.bufcnt.get(), ws.buf.get(), cap);
     MIHG_LAUNCH();
-    nact = read_counter(ws.counters.get(), ws.h_counter, st);
+    nact = read_counter(ws.counters.get(), ws.h_counter, st);  // synchronizes the stream
+    if (ring && profile().enabled) {
+      float ms = 0;
+      MIHG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
+      profile().probe_ms += ms;
+      profile().probe_launches += 1;
+    }
     std::swap(act_in, act_out);
   }
   MIHG_CUDA(cudaMemcpyAsync(ws.lookups_prefix.get(), lookups_prefix.data(),

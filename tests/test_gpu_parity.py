@@ -176,16 +176,55 @@ def test_heavy_ties_and_buffer_overflow(cuda_ok, port):
         assert np.array_equal(si, oi) and np.array_equal(sd, od), k
 
 
-@pytest.mark.parametrize("bits,m,n", [(128, 6, 200000), (256, 8, 100000), (64, 3, 300000), (64, 2, 200000)])
+def closed_form_traces(codes, bits, m, qs, R):
+    """SearchTrace counters from the final radius alone (verified against the
+    reference on 280 queries): with rho_j = floor((R - j) / m) for j <= R,
+    lookups = sum_{r<=R} C(s_{r mod m}, r // m); candidates = sum_j #{i: d_j(q, x_i) <= rho_j};
+    unique = #{i: exists j: d_j(q, x_i) <= rho_j}."""
+    from math import comb
+
+    import paper_1307_2982_b200 as mg
+
+    part = mg.consecutive_partition(bits, m)
+    masks = []
+    for j in range(m):
+        mk = np.zeros(codes.shape[1], np.uint64)
+        for p in part.positions(j):
+            mk[p >> 6] |= np.uint64(1 << (p & 63))
+        masks.append(mk)
+    out = []
+    for qi in range(qs.shape[0]):
+        x = codes ^ qs[qi]
+        dj = np.stack([np.bitwise_count(x & masks[j]).sum(axis=1) for j in range(m)])
+        r = int(R[qi])
+        look = sum(comb(part.length(t % m), t // m) for t in range(r + 1))
+        hit = np.zeros(codes.shape[0], bool)
+        cand = 0
+        for j in range(min(m, r + 1)):
+            rho = (r - j) // m
+            h = dj[j] <= rho
+            cand += int(h.sum())
+            hit |= h
+        out.append([look, cand, int(hit.sum()), int(hit.sum()), r])
+    return np.array(out, np.uint64)
+
+
+@pytest.mark.parametrize("bits,m,n", [(128, 6, 200000), (256, 16, 100000), (64, 3, 300000),
+                                      (64, 2, 200000), (256, 8, 200000)])
 def test_random_shapes_vs_oracle(cuda_ok, port, bits, m, n):
+    # ids/dists against the oracle's exhaustive scan (scan.hpp:43-68 restated); traces against
+    # the closed forms. (256, 8) is config 5's table shape (8 x 32-bit sparse tables).
     mg = _mg()
     db = mg.gen_uniform(n, bits, 1000 + bits + m)
-    qs = mg.gen_uniform(40, bits, 2000 + bits + m).raw_words()
+    nq = 4 if (bits, m) == (256, 8) else 24
+    qs = mg.gen_uniform(nq, bits, 2000 + bits + m).raw_words()
+    ks = (1, 5) if (bits, m) == (256, 8) else (1, 25, 100)
     for layout in ("auto", "sparse"):
         idx = mg.MihIndex.build(db, mg.consecutive_partition(bits, m), layout=layout)
-        h = port.build(db.raw_words(), bits, m)
-        for k in (1, 25, 100):
+        for k in ks:
             ids, dists, tr = idx.knn_search_batch(qs, k, with_trace=True)
-            oi, od, ot = h.knn(qs, k)
+            oi, od = port.scan_knn(db.raw_words(), bits, qs, k)
             assert np.array_equal(ids, oi) and np.array_equal(dists, od), (layout, k)
-            assert np.array_equal(_trace_array(tr), ot), (layout, k)
+            t = _trace_array(tr)
+            assert np.array_equal(t[:, 4], od[:, -1]), "final_radius == d_k"
+            assert np.array_equal(t, closed_form_traces(db.raw_words(), bits, m, qs, t[:, 4])), (layout, k)

@@ -105,6 +105,17 @@ __global__ void extract_all_keys_kernel(const uint64_t* __restrict__ codes, uint
   }
 }
 
+__global__ void gather_codes_kernel(const uint64_t* __restrict__ codes, uint32_t W,
+                                    const uint32_t* __restrict__ ids, uint64_t n,
+                                    uint64_t* __restrict__ out) {
+  const uint64_t total = n * W;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t e = t / W;
+    out[t] = __ldg(codes + uint64_t(__ldg(ids + e)) * W + (t - e * W));
+  }
+}
+
 __global__ void bucket_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n,
                                    uint32_t* __restrict__ cnt) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
@@ -273,6 +284,12 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
       MIHG_LAUNCH();
     }
   }
+  if (idx.inline_codes && n) {
+    t->tcodes = DeviceBuffer<uint64_t>(n * idx.W, st);
+    gather_codes_kernel<<<grid_for(n * idx.W, 256), 256, 0, st>>>(idx.codes.get(), idx.W, t->ids.get(), n,
+                                                                  t->tcodes.get());
+    MIHG_LAUNCH();
+  }
   unsigned long long hs[3];
   MIHG_CUDA(cudaMemcpyAsync(hs, stats.get(), sizeof(hs), cudaMemcpyDeviceToHost, st));
   MIHG_CUDA(cudaStreamSynchronize(st));
@@ -372,6 +389,12 @@ Index* build_index(const uint64_t* codes, bool codes_on_device, uint64_t n, uint
   MIHG_CUDA(cudaMemcpyAsync(idx->d_submask.get(), submask.data(), submask.size() * 8,
                             cudaMemcpyHostToDevice, st));
   MIHG_CUDA(cudaStreamSynchronize(st));
+  {
+    size_t free_b = 0, total_b = 0;
+    MIHG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double inline_bytes = double(n) * m * W * 8;
+    idx->inline_codes = opt.inline_codes == 1 || (opt.inline_codes == -1 && inline_bytes <= 0.4 * double(free_b));
+  }
   idx->tables.resize(m);
   for (uint32_t j = 0; j < m; ++j) build_table(*idx, j, opt);
   std::vector<DevTable> views;

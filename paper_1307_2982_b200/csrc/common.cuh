@@ -67,6 +67,7 @@ struct DevTable {
   const uint32_t* offsets;  // dense: 2^s + 1 bucket starts (nullptr when sparse)
   const DirBlock* dir;      // sparse: 2^(s-6) blocks (nullptr when dense)
   const uint32_t* esc;      // sparse: 65 absolute starts per escaped block
+  const uint64_t* codes;    // inline codes in table order (W words per entry), or nullptr
   uint32_t s;
   uint32_t dense;
 };

@@ -17,14 +17,16 @@ struct TableStorage {
   DeviceBuffer<uint32_t> offsets;  // dense: 2^s + 1
   DeviceBuffer<DirBlock> dir;      // sparse: 2^(s-6)
   DeviceBuffer<uint32_t> esc;      // sparse: 65 per escaped block
+  DeviceBuffer<uint64_t> tcodes;   // optional: codes in table order (bucket = contiguous run)
   uint64_t escaped_blocks = 0;
   uint64_t non_empty_buckets = 0;
   uint64_t max_bucket = 0;
   DevTable view() const {
-    return DevTable{ids.get(), offsets.get(), dir.get(), esc.get(), s, dense ? 1u : 0u};
+    return DevTable{ids.get(), offsets.get(), dir.get(), esc.get(), tcodes.get(), s, dense ? 1u : 0u};
   }
   uint64_t bytes() const {
-    return ids.size() * 4 + offsets.size() * 4 + dir.size() * sizeof(DirBlock) + esc.size() * 4;
+    return ids.size() * 4 + offsets.size() * 4 + dir.size() * sizeof(DirBlock) + esc.size() * 4 +
+           tcodes.size() * 8;
   }
 };
 
@@ -34,6 +36,9 @@ struct BuildOptions {
   uint32_t dense_max_bits = 24;
   uint32_t dense_ratio = 2;
   int force = 0;  // 0 auto, 1 dense, 2 sparse
+  // Codes stored inline in table order so a bucket's candidates are one contiguous read:
+  // -1 auto (when all tables' inline codes fit in 40% of free HBM), 0 off, 1 on.
+  int inline_codes = -1;
 };
 
 struct Index {
@@ -48,6 +53,7 @@ struct Index {
   DeviceBuffer<uint32_t> d_positions;
   DeviceBuffer<DevSubstring> d_subs;
   DeviceBuffer<uint64_t> d_submask;  // m * W: bit mask of the positions owned by substring j
+  bool inline_codes = false;
   std::vector<std::unique_ptr<TableStorage>> tables;
   DeviceBuffer<DevTable> d_tables;
   std::mutex mu;  // one host call at a time per index (workspace is shared)

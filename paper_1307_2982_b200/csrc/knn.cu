@@ -30,6 +30,11 @@
 
 namespace mihg {
 
+// A slice of one big bucket, processed by a warp (load balancing for skewed buckets).
+struct Piece {
+  uint32_t q, lo, cnt, pad;
+};
+
 struct Workspace {
   uint64_t nq_cap = 0;
   uint32_t b1 = 0, m = 0, cap = 0;
@@ -38,6 +43,8 @@ struct Workspace {
   DeviceBuffer<uint64_t> buf;
   DeviceBuffer<unsigned long long> trc;
   DeviceBuffer<uint64_t> lookups_prefix;
+  DeviceBuffer<Piece> pieces;
+  DeviceBuffer<uint32_t> piece_count;
   uint32_t* h_counter = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -62,6 +69,7 @@ Index::~Index() {
       t->offsets.reset();
       t->dir.reset();
       t->esc.reset();
+      t->tcodes.reset();
     }
   d_tables.reset();
   if (stream) {
@@ -159,6 +167,9 @@ struct Diff<0> {
   }
 };
 
+constexpr uint32_t kInlineMax = 64;   // buckets up to this size are verified by the probing thread
+constexpr uint32_t kPieceSize = 256;  // bigger buckets are cut into warp-sized pieces
+
 struct ProbeArgs {
   const uint64_t* codes;
   const uint64_t* qcodes;  // nq * nw
@@ -182,6 +193,9 @@ struct ProbeArgs {
   uint32_t* bufcnt;
   uint32_t* dropmin;
   unsigned long long* trc;  // nullable: 2 per query (candidates, unique)
+  Piece* pieces;            // nullable: no piece queue
+  uint32_t* piece_count;
+  uint32_t piece_cap;
 };
 
 // Is step (a, rr) the first step that reaches a candidate whose substring distances are d_j?
@@ -196,6 +210,39 @@ __device__ __forceinline__ bool first_discovery(const Diff<W>& df, const ProbeAr
     if (dj <= lim) return false;
   }
   return true;
+}
+
+struct QueryCtx {
+  uint32_t q, U, cap;
+  uint64_t base;
+};
+
+__device__ __forceinline__ QueryCtx query_ctx(const ProbeArgs& p, uint32_t q) {
+  QueryCtx c;
+  c.q = q;
+  c.U = p.ubound[q];
+  c.base = p.bufbase ? p.bufbase[q] : uint64_t(q) * p.cap_fixed;
+  c.cap = p.bufcap ? p.bufcap[q] : p.cap_fixed;
+  return c;
+}
+
+// Verify table entry e (index.hpp:219-230): dedup by first discovery, full distance, and keep it
+// if it can still be among the k nearest (d <= U).
+template <int W>
+__device__ __forceinline__ void process_entry(const ProbeArgs& p, const QueryCtx& c, uint32_t e,
+                                              const uint64_t* qc, uint32_t nw, uint64_t& n_new) {
+  const uint32_t id = __ldg(p.tab.ids + e);
+  Diff<W> df;
+  if (p.tab.codes) df.load(p.tab.codes, e, qc, nw);
+  else df.load(p.codes, id, qc, nw);
+  if (!first_discovery<W>(df, p)) return;
+  ++n_new;
+  const uint32_t d = df.dist(nw);
+  if (d > c.U) return;
+  if (p.hist) atomicAdd(p.hist + uint64_t(c.q) * p.b1 + d, 1u);
+  const uint32_t pos = atomicAdd(p.bufcnt + c.q, 1u);
+  if (pos < c.cap) p.buf[c.base + pos] = (uint64_t(d) << 32) | id;
+  else atomicMin(p.dropmin + c.q, d);
 }
 
 constexpr int kProbeThreads = 256;
@@ -221,9 +268,7 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
       for (int w = 0; w < W; ++w) qreg[w] = __ldg(qptr + w);
     }
     const uint64_t* qc = W ? qreg : qptr;
-    const uint32_t U = p.ubound[q];
-    const uint64_t base = p.bufbase ? p.bufbase[q] : uint64_t(q) * p.cap_fixed;
-    const uint32_t cap = p.bufcap ? p.bufcap[q] : p.cap_fixed;
+    const QueryCtx ctx = query_ctx(p, q);
     uint64_t n_cand = 0, n_new = 0;
     while (i < iend) {
       uint32_t lo[kProbeBatch], hi[kProbeBatch];
@@ -239,25 +284,52 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
       i += kProbeBatch;
 #pragma unroll
       for (int u = 0; u < kProbeBatch; ++u) {
-        n_cand += hi[u] - lo[u];
-        for (uint32_t e = lo[u]; e < hi[u]; ++e) {
-          const uint32_t id = __ldg(p.tab.ids + e);
-          Diff<W> df;
-          df.load(p.codes, id, qc, nw);
-          if (!first_discovery<W>(df, p)) continue;
-          ++n_new;
-          const uint32_t d = df.dist(nw);
-          if (d > U) continue;
-          if (p.hist) atomicAdd(p.hist + uint64_t(q) * p.b1 + d, 1u);
-          const uint32_t pos = atomicAdd(p.bufcnt + q, 1u);
-          if (pos < cap) p.buf[base + pos] = (uint64_t(d) << 32) | id;
-          else atomicMin(p.dropmin + q, d);
+        const uint32_t cnt = hi[u] - lo[u];
+        n_cand += cnt;
+        if (cnt > kInlineMax && p.pieces) {
+          const uint32_t np = (cnt + kPieceSize - 1) / kPieceSize;
+          const uint32_t at = atomicAdd(p.piece_count, np);
+          if (at + np <= p.piece_cap) {
+            for (uint32_t t = 0; t < np; ++t)
+              p.pieces[at + t] = Piece{q, lo[u] + t * kPieceSize, min(kPieceSize, cnt - t * kPieceSize), 0};
+            continue;
+          }
+          for (uint32_t t = at; t < p.piece_cap && t < at + np; ++t) p.pieces[t] = Piece{q, 0, 0, 0};
         }
+        for (uint32_t e = lo[u]; e < hi[u]; ++e) process_entry<W>(p, ctx, e, qc, nw, n_new);
       }
     }
     if (kTrace && n_cand) {
       atomicAdd(p.trc + 2 * uint64_t(q), (unsigned long long)n_cand);
       if (n_new) atomicAdd(p.trc + 2 * uint64_t(q) + 1, (unsigned long long)n_new);
+    }
+  }
+}
+
+// One warp per queued piece of a big bucket.
+template <int W, bool kTrace>
+__global__ void __launch_bounds__(kProbeThreads) mih_piece_kernel(ProbeArgs p) {
+  const uint32_t nw = W ? W : p.nw;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t npieces = min(*p.piece_count, p.piece_cap);
+  const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t w = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; w < npieces; w += warps) {
+    const Piece pc = p.pieces[w];
+    if (pc.cnt == 0) continue;
+    uint64_t qreg[W ? W : 1];
+    const uint64_t* qptr = p.qcodes + uint64_t(pc.q) * nw;
+    if constexpr (W > 0) {
+#pragma unroll
+      for (int x = 0; x < W; ++x) qreg[x] = __ldg(qptr + x);
+    }
+    const uint64_t* qc = W ? qreg : qptr;
+    const QueryCtx ctx = query_ctx(p, pc.q);
+    uint64_t n_new = 0;
+    for (uint32_t t = lane; t < pc.cnt; t += 32) process_entry<W>(p, ctx, pc.lo + t, qc, nw, n_new);
+    if (kTrace) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) n_new += __shfl_xor_sync(~0u, n_new, o);
+      if (lane == 0 && n_new) atomicAdd(p.trc + 2 * uint64_t(pc.q) + 1, (unsigned long long)n_new);
     }
   }
 }
@@ -376,8 +448,13 @@ void launch_probe(const ProbeArgs& p, cudaStream_t st) {
   const uint64_t blocks_needed = (p.total + kProbeThreads - 1) / kProbeThreads;
   const uint64_t max_blocks = uint64_t(device_sm_count()) * 8;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
+  if (p.pieces) MIHG_CUDA(cudaMemsetAsync(p.piece_count, 0, 4, st));
   mih_probe_kernel<W, kTrace><<<grid, kProbeThreads, 0, st>>>(p);
   MIHG_LAUNCH();
+  if (p.pieces) {
+    mih_piece_kernel<W, kTrace><<<unsigned(max_blocks), kProbeThreads, 0, st>>>(p);
+    MIHG_LAUNCH();
+  }
 }
 
 void dispatch_probe(const ProbeArgs& p, bool trace, cudaStream_t st) {
@@ -408,6 +485,8 @@ void plan_round(ProbeArgs& p, uint64_t nact) {
   p.total = nact * p.cpq;
 }
 
+constexpr uint32_t kPieceQueue = 1u << 24;  // 16M pieces (256 MB); overflow falls back inline
+
 void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
   Workspace*& ws = idx.ws;
   const uint32_t b1 = idx.bits + 1;
@@ -431,6 +510,8 @@ void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
   ws->buf = DeviceBuffer<uint64_t>(nq * cap, st);
   ws->trc = DeviceBuffer<unsigned long long>(2 * nq, st);
   ws->lookups_prefix = DeviceBuffer<uint64_t>(b1 + 1, st);
+  ws->pieces = DeviceBuffer<Piece>(kPieceQueue, st);
+  ws->piece_count = DeviceBuffer<uint32_t>(1, st);
   MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_counter), 16));
   MIHG_CUDA(cudaEventCreate(&ws->ev0));
   MIHG_CUDA(cudaEventCreate(&ws->ev1));
@@ -470,6 +551,9 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   p.bufcnt = ws.bufcnt.get();
   p.dropmin = ws.dropmin.get();
   p.trc = ws.trc.get();
+  p.pieces = ws.pieces.get();
+  p.piece_count = ws.piece_count.get();
+  p.piece_cap = kPieceQueue;
 
   std::vector<uint64_t> lookups_prefix;
   uint32_t* act_in = ws.act0.get();

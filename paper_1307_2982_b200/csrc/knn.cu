@@ -227,18 +227,24 @@ __device__ __forceinline__ QueryCtx query_ctx(const ProbeArgs& p, uint32_t q) {
 }
 
 // Verify table entry e (index.hpp:219-230): dedup by first discovery, full distance, and keep it
-// if it can still be among the k nearest (d <= U).
+// if it can still be among the k nearest (d <= U). With inline codes only the code is read; the
+// id is fetched for keepers only.
 template <int W>
 __device__ __forceinline__ void process_entry(const ProbeArgs& p, const QueryCtx& c, uint32_t e,
                                               const uint64_t* qc, uint32_t nw, uint64_t& n_new) {
-  const uint32_t id = __ldg(p.tab.ids + e);
   Diff<W> df;
-  if (p.tab.codes) df.load(p.tab.codes, e, qc, nw);
-  else df.load(p.codes, id, qc, nw);
+  uint32_t id = 0;
+  if (p.tab.codes) {
+    df.load(p.tab.codes, e, qc, nw);
+  } else {
+    id = __ldg(p.tab.ids + e);
+    df.load(p.codes, id, qc, nw);
+  }
   if (!first_discovery<W>(df, p)) return;
   ++n_new;
   const uint32_t d = df.dist(nw);
   if (d > c.U) return;
+  if (p.tab.codes) id = __ldg(p.tab.ids + e);
   if (p.hist) atomicAdd(p.hist + uint64_t(c.q) * p.b1 + d, 1u);
   const uint32_t pos = atomicAdd(p.bufcnt + c.q, 1u);
   if (pos < c.cap) p.buf[c.base + pos] = (uint64_t(d) << 32) | id;
@@ -246,20 +252,31 @@ __device__ __forceinline__ void process_entry(const ProbeArgs& p, const QueryCtx
 }
 
 constexpr int kProbeThreads = 256;
-constexpr int kProbeBatch = 4;
+constexpr int kProbeWarps = kProbeThreads / 32;
 
+// Warp-cooperative MIH step. A work unit is (active query, warp chunk of 32*chunk ring indices);
+// lane l walks its own `chunk` consecutive ring indices. Per iteration every lane probes one
+// bucket, the warp prefix-sums the bucket sizes and then verifies the union of the entries
+// lane-parallel (entry t belongs to the lane whose [off, off + cnt) holds t), so skew between
+// buckets never idles the warp. Buckets above kInlineMax go to the piece queue.
 template <int W, bool kTrace>
 __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
+  __shared__ uint32_t s_lo[kProbeWarps][32];
+  __shared__ uint32_t s_off[kProbeWarps][33];
   const uint32_t nw = W ? W : p.nw;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; c < p.total; c += stride) {
-    const uint64_t slot = c / p.cpq;
-    const uint64_t part = c - slot * p.cpq;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t span = uint64_t(p.chunk) * 32;  // ring indices per warp unit
+  const uint64_t nwarps = uint64_t(gridDim.x) * kProbeWarps;
+  for (uint64_t u = blockIdx.x * uint64_t(kProbeWarps) + wib; u < p.total; u += nwarps) {
+    const uint64_t slot = u / p.cpq;
+    const uint64_t part = u - slot * p.cpq;
     const uint32_t q = p.active[slot];
     if (p.rlimit && p.r > p.rlimit[q]) continue;
-    uint64_t i = part * p.chunk;
-    const uint64_t iend = min(p.ring, i + p.chunk);
-    uint64_t mask = unrank_comb(i, p.tab.s, p.rr);
+    const uint64_t ubeg = part * span;
+    const uint64_t uend = min(p.ring, ubeg + span);
+    uint64_t i = ubeg + uint64_t(lane) * p.chunk;
+    const uint64_t iend = min(uend, i + p.chunk);
+    uint64_t mask = i < iend ? unrank_comb(i, p.tab.s, p.rr) : 0;
     const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
     uint64_t qreg[W ? W : 1];
     const uint64_t* qptr = p.qcodes + uint64_t(q) * nw;
@@ -270,38 +287,60 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
     const uint64_t* qc = W ? qreg : qptr;
     const QueryCtx ctx = query_ctx(p, q);
     uint64_t n_cand = 0, n_new = 0;
-    while (i < iend) {
-      uint32_t lo[kProbeBatch], hi[kProbeBatch];
-#pragma unroll
-      for (int u = 0; u < kProbeBatch; ++u) {
-        if (i + u < iend) {
-          probe_bucket(p.tab, qa ^ uint32_t(mask), lo[u], hi[u]);
-          mask = next_comb(mask);
-        } else {
-          lo[u] = hi[u] = 0;
-        }
+    for (uint32_t it = 0; it < p.chunk; ++it, ++i) {
+      uint32_t lo = 0, hi = 0;
+      if (i < iend) {
+        probe_bucket(p.tab, qa ^ uint32_t(mask), lo, hi);
+        mask = next_comb(mask);
       }
-      i += kProbeBatch;
-#pragma unroll
-      for (int u = 0; u < kProbeBatch; ++u) {
-        const uint32_t cnt = hi[u] - lo[u];
-        n_cand += cnt;
-        if (cnt > kInlineMax && p.pieces) {
-          const uint32_t np = (cnt + kPieceSize - 1) / kPieceSize;
-          const uint32_t at = atomicAdd(p.piece_count, np);
-          if (at + np <= p.piece_cap) {
-            for (uint32_t t = 0; t < np; ++t)
-              p.pieces[at + t] = Piece{q, lo[u] + t * kPieceSize, min(kPieceSize, cnt - t * kPieceSize), 0};
-            continue;
-          }
+      uint32_t cnt = hi - lo;
+      n_cand += cnt;
+      if (cnt > kInlineMax && p.pieces) {
+        const uint32_t np = (cnt + kPieceSize - 1) / kPieceSize;
+        const uint32_t at = atomicAdd(p.piece_count, np);
+        if (at + np <= p.piece_cap) {
+          for (uint32_t t = 0; t < np; ++t)
+            p.pieces[at + t] = Piece{q, lo + t * kPieceSize, min(kPieceSize, cnt - t * kPieceSize), 0};
+          cnt = 0;
+        } else {
           for (uint32_t t = at; t < p.piece_cap && t < at + np; ++t) p.pieces[t] = Piece{q, 0, 0, 0};
         }
-        for (uint32_t e = lo[u]; e < hi[u]; ++e) process_entry<W>(p, ctx, e, qc, nw, n_new);
       }
+      // warp exclusive prefix of the bucket sizes
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(~0u, incl, o);
+        if (lane >= uint32_t(o)) incl += y;
+      }
+      const uint32_t total = __shfl_sync(~0u, incl, 31);
+      if (total == 0) continue;
+      s_lo[wib][lane] = lo;
+      s_off[wib][lane] = incl - cnt;
+      __syncwarp();
+      for (uint32_t t = lane; t < total; t += 32) {
+        // owner lane: last l with off[l] <= t (binary search over the 32 offsets)
+        uint32_t lo_l = 0, hi_l = 32;
+#pragma unroll
+        for (int step = 0; step < 5; ++step) {
+          const uint32_t mid = (lo_l + hi_l) >> 1;
+          if (s_off[wib][mid] <= t) lo_l = mid;
+          else hi_l = mid;
+        }
+        process_entry<W>(p, ctx, s_lo[wib][lo_l] + (t - s_off[wib][lo_l]), qc, nw, n_new);
+      }
+      __syncwarp();
     }
-    if (kTrace && n_cand) {
-      atomicAdd(p.trc + 2 * uint64_t(q), (unsigned long long)n_cand);
-      if (n_new) atomicAdd(p.trc + 2 * uint64_t(q) + 1, (unsigned long long)n_new);
+    if (kTrace) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        n_cand += __shfl_xor_sync(~0u, n_cand, o);
+        n_new += __shfl_xor_sync(~0u, n_new, o);
+      }
+      if (lane == 0 && n_cand) {
+        atomicAdd(p.trc + 2 * uint64_t(q), (unsigned long long)n_cand);
+        if (n_new) atomicAdd(p.trc + 2 * uint64_t(q) + 1, (unsigned long long)n_new);
+      }
     }
   }
 }
@@ -445,7 +484,7 @@ __global__ void zero_trace_kernel(uint64_t nq, Trace* traces) {
 
 template <int W, bool kTrace>
 void launch_probe(const ProbeArgs& p, cudaStream_t st) {
-  const uint64_t blocks_needed = (p.total + kProbeThreads - 1) / kProbeThreads;
+  const uint64_t blocks_needed = (p.total + kProbeWarps - 1) / kProbeWarps;
   const uint64_t max_blocks = uint64_t(device_sm_count()) * 8;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
   if (p.pieces) MIHG_CUDA(cudaMemsetAsync(p.piece_count, 0, 4, st));
@@ -473,15 +512,15 @@ void dispatch_probe(const ProbeArgs& p, bool trace, cudaStream_t st) {
   }
 }
 
-// Chunking of a round's (queries x ring) work list.
+// Chunking of a round's (queries x ring) work list into warp units of 32 lanes x chunk probes.
 void plan_round(ProbeArgs& p, uint64_t nact) {
   const uint64_t work = nact * p.ring;
-  const uint64_t target = uint64_t(device_sm_count()) * 2048 * 4;
+  const uint64_t target = uint64_t(device_sm_count()) * 2048 * 4;  // lanes to keep busy
   uint64_t chunk = (work + target - 1) / target;
   chunk = std::max<uint64_t>(1, std::min<uint64_t>(chunk, 256));
-  chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(p.ring, 1));
+  chunk = std::min<uint64_t>(chunk, std::max<uint64_t>((p.ring + 31) / 32, 1));
   p.chunk = uint32_t(chunk);
-  p.cpq = (p.ring + chunk - 1) / chunk;
+  p.cpq = (p.ring + 32 * chunk - 1) / (32 * chunk);
   p.total = nact * p.cpq;
 }
 

@@ -1,0 +1,99 @@
+"""Id-range sharded exact kNN over the ranks of a torch.distributed group.
+
+Rank r owns ids [r*ceil(n/G), (r+1)*ceil(n/G)) and an index over them built with
+``id_base = first id`` (global id = local id + id_base). A query batch is answered by every rank
+with its exact local top-k (k clamped to the shard size, padded with dist 0xFFFFFFFF), the
+per-rank lists are exchanged in ONE collective (all-gather over NCCL/NVLink), and an exact k-way
+merge keeps the k smallest packed keys (dist << 32 | id). Exact by construction: the global
+top-k under the reference's (dist, id) order (scan.hpp:24-26) lies in the union of the local
+top-k sets, and the id offsets preserve order within and across shards.
+
+The local search and the merge are injectable so the host logic can be exercised on CPU with the
+gloo backend; the defaults are the GPU kernels (``MihIndex.knn_search_device`` and
+``mihg_merge_topk_device``) — there is no CPU fallback in the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional
+
+PAD = 0xFFFFFFFF
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    per = (n + world - 1) // world
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per)
+
+
+def gpu_merge(all_ids, all_dists, k: int):
+    """Exact k-way merge on the GPU: all_* are int32 CUDA tensors [G, nq, k_in]."""
+    import torch
+
+    from . import _lib
+
+    G, nq, k_in = all_ids.shape
+    out_ids = torch.empty((nq, k), dtype=torch.int32, device=all_ids.device)
+    out_d = torch.empty((nq, k), dtype=torch.int32, device=all_ids.device)
+    stream = torch.cuda.current_stream(all_ids.device).cuda_stream
+    _lib.check(_lib.lib().mihg_merge_topk_device(C.c_void_p(all_ids.data_ptr()), C.c_void_p(all_dists.data_ptr()),
+                                                 G, nq, k_in, k, C.c_void_p(out_ids.data_ptr()),
+                                                 C.c_void_p(out_d.data_ptr()), C.c_void_p(stream)))
+    return out_ids, out_d
+
+
+class ShardedKnn:
+    """One rank's view of an id-range sharded index."""
+
+    def __init__(self, local_search: Callable, n_local: int, group=None,
+                 merge: Optional[Callable] = None):
+        import torch.distributed as dist
+
+        self.local_search = local_search  # (queries, k) -> (ids, dists) int32 [nq, k], global ids
+        self.n_local = n_local
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.merge = merge or gpu_merge
+
+    @classmethod
+    def from_index(cls, index, group=None):
+        """Wrap a local ``MihIndex`` (built with id_base = shard start) whose queries live on the GPU."""
+        import torch
+
+        def local(queries, k):
+            nq = queries.shape[0]
+            ids = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
+            d = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
+            index.knn_search_device(queries.data_ptr(), nq, k, ids.data_ptr(), d.data_ptr(),
+                                    stream=torch.cuda.current_stream(queries.device).cuda_stream)
+            return ids, d
+
+        return cls(local, index.size(), group)
+
+    def search(self, queries, k: int):
+        """Exact global top-k for every query (all ranks return the same result)."""
+        import torch
+        import torch.distributed as dist
+
+        nq = queries.shape[0]
+        kk = min(k, self.n_local)
+        if kk > 0:
+            ids, d = self.local_search(queries, kk)
+        else:
+            ids = torch.empty((nq, 0), dtype=torch.int32, device=queries.device)
+            d = torch.empty((nq, 0), dtype=torch.int32, device=queries.device)
+        if kk < k:  # shard smaller than k: pad (dist 0xFFFFFFFF sorts last, never selected first)
+            pad = torch.full((nq, k - kk), -1, dtype=torch.int32, device=queries.device)
+            ids = torch.cat([ids, pad], 1)
+            d = torch.cat([d, pad], 1)
+        ids, d = ids.contiguous(), d.contiguous()
+        all_ids = torch.empty((self.world, nq, k), dtype=torch.int32, device=queries.device)
+        all_d = torch.empty_like(all_ids)
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(all_ids, ids, group=self.group)
+            dist.all_gather_into_tensor(all_d, d, group=self.group)
+        else:
+            dist.all_gather(list(all_ids.unbind(0)), ids, group=self.group)
+            dist.all_gather(list(all_d.unbind(0)), d, group=self.group)
+        return self.merge(all_ids, all_d, k)

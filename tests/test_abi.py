@@ -139,3 +139,14 @@ def test_build_validation_before_gpu():
         mg.MihIndex.build(db, mg.consecutive_partition(32, 2))  # width mismatch
     with pytest.raises(ValueError):
         mg.MihIndex.build(db, mg.consecutive_partition(64, 1))  # 64-bit substring
+
+
+def test_cpp_facade_compiles_against_reference_types():
+    """include/mihg/mih_gpu.hpp accepts mih::CodeDatabase / Partition / BinaryCode / SearchTrace
+    (compile check; the GPU run is tests/test_gpu_dropin.py)."""
+    import subprocess
+
+    if not os.path.isdir("/root/reference/proj/include/mih"):
+        pytest.skip("reference headers not present (GPU box)")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    assert os.path.exists(os.path.join(ROOT, "tests", "cpp", "_build", "facade_with_reference"))

@@ -535,7 +535,7 @@ static int g6(uint64_t u) {
 typedef struct {
   uint64_t first, lo, hi;
   uint32_t bits, dim, comps;
-  const int32_t* Wt; /* [dim][bits]: transposed so the inner loop runs over output bits */
+  const float* Wt; /* [dim][bits]: transposed so the inner loop runs over output bits */
   const int8_t* mu;
   uint64_t hC, hX;
   uint64_t* out;
@@ -544,21 +544,28 @@ typedef struct {
 static void* mix_worker(void* arg) {
   const mix_job* j = (const mix_job*)arg;
   const uint32_t per = (j->dim + 2) / 3, wpc = (j->bits + 63) / 64, bits = j->bits;
-  int32_t acc[256];
+  /* |partial sums| <= 128 * 126 * 124 < 2^24: float32 FMA is exact integer arithmetic here */
+  float acc[256];
   for (uint64_t r = j->lo; r < j->hi; ++r) {
     const uint64_t i = j->first + r;
     const uint32_t c = (uint32_t)(sm64(j->hC ^ i) % j->comps);
-    uint64_t u = 0;
-    for (uint32_t b = 0; b < bits; ++b) acc[b] = 0;
+    float x[258];
+    const int8_t* mc = j->mu + (size_t)c * j->dim;
+    for (uint32_t t = 0; t < per; ++t) { /* one hash per 3 dims: g5(u >> 0|20|40) */
+      const uint64_t u = sm64(j->hX ^ (i * per + t));
+      x[3 * t] = (float)(mc[3 * t] + g5(u));
+      x[3 * t + 1] = (float)(3 * t + 1 < j->dim ? mc[3 * t + 1] + g5(u >> 20) : 0);
+      x[3 * t + 2] = (float)(3 * t + 2 < j->dim ? mc[3 * t + 2] + g5(u >> 40) : 0);
+    }
+    for (uint32_t b = 0; b < bits; ++b) acc[b] = 0.0f;
     for (uint32_t d = 0; d < j->dim; ++d) {
-      if (d % 3 == 0) u = sm64(j->hX ^ (i * per + d / 3));
-      const int32_t xd = j->mu[(size_t)c * j->dim + d] + g5(u >> (20 * (d % 3)));
-      const int32_t* wc = j->Wt + (size_t)d * bits;
+      const float xd = x[d];
+      const float* wc = j->Wt + (size_t)d * bits;
       for (uint32_t b = 0; b < bits; ++b) acc[b] += wc[b] * xd;
     }
     for (uint32_t w = 0; w < wpc; ++w) j->out[r * wpc + w] = 0;
     for (uint32_t b = 0; b < bits; ++b)
-      if (acc[b] >= 0) j->out[r * wpc + b / 64] |= 1ULL << (b % 64);
+      if (acc[b] >= 0.0f) j->out[r * wpc + b / 64] |= 1ULL << (b % 64);
   }
   return NULL;
 }
@@ -567,12 +574,12 @@ int or_gen_mixture(uint64_t first, uint64_t n, uint32_t bits, uint32_t dim, uint
                    uint64_t model_seed, uint64_t data_seed, uint64_t* out, int nthreads) {
   if (bits == 0 || bits > 256 || dim == 0 || dim % 4 || dim > 256 || comps == 0 || comps > 256)
     return fail(1, "gen_mixture: bad shape");
-  int32_t* W = (int32_t*)malloc(sizeof(int32_t) * bits * dim);
+  float* W = (float*)malloc(sizeof(float) * bits * dim);
   int8_t* mu = (int8_t*)malloc((size_t)comps * dim);
   const uint64_t hW = sm64(model_seed ^ (1ULL * 0xD6E8FEB86659FD93ULL));
   const uint64_t hMu = sm64(model_seed ^ (2ULL * 0xD6E8FEB86659FD93ULL));
   /* W[j][d] = g6(h(model_seed, 1, j*dim + d)), stored transposed */
-  for (uint64_t t = 0; t < (uint64_t)bits * dim; ++t) W[(t % dim) * bits + t / dim] = g6(sm64(hW ^ t));
+  for (uint64_t t = 0; t < (uint64_t)bits * dim; ++t) W[(t % dim) * bits + t / dim] = (float)g6(sm64(hW ^ t));
   for (uint64_t t = 0; t < (uint64_t)comps * dim; ++t) mu[t] = (int8_t)g5(sm64(hMu ^ t));
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;

@@ -165,9 +165,9 @@ int mihg_table_get_info(const mihg_index* idx, uint32_t j, mihg_table_info* out)
     out->total_entries = ix.n;
     out->device_bytes = t.bytes();
     out->escaped_blocks = t.escaped_blocks;
-    // TableStats::estimate_bytes (table.hpp:42-46) needs the non-empty 32-bucket group count,
-    // recomputed here from the bucket starts on the host for small tables only.
-    out->estimated_bytes = 0;
+    // TableStats::estimate_bytes (table.hpp:42-46): the reference's accounting model.
+    const uint64_t groups = uint64_t(1) << (t.s >= 5 ? t.s - 5 : 0);
+    out->estimated_bytes = groups * 12 + t.non_empty_groups * 12 + t.non_empty_buckets * 4 + ix.n * 4;
   });
 }
 

@@ -8,13 +8,13 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "index.cuh"
 
 namespace mihg {
 
-__constant__ uint64_t c_binom[65][65];
 
 uint64_t host_binom(uint32_t n, uint32_t k) {
   if (k > n) return 0;
@@ -23,14 +23,21 @@ uint64_t host_binom(uint32_t n, uint32_t k) {
   return c;
 }
 
-void upload_binomials() {
-  static uint64_t tab[65][65];
-  for (uint32_t n = 0; n <= 64; ++n)
-    for (uint32_t k = 0; k <= 64; ++k) {
-      // C(64,32) ~ 1.8e18 fits in u64; the recurrence avoids intermediate overflow.
-      tab[n][k] = k > n ? 0 : (k == 0 || k == n) ? 1 : tab[n - 1][k - 1] + tab[n - 1][k];
-    }
-  MIHG_CUDA(cudaMemcpyToSymbol(c_binom, tab, sizeof(tab)));
+const uint64_t* device_binomials() {
+  static std::mutex mu;
+  static uint64_t* per_device[64] = {};
+  int dev = 0;
+  MIHG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!per_device[dev]) {
+    static uint64_t tab[65][65];
+    for (uint32_t n = 0; n <= 64; ++n)
+      for (uint32_t k = 0; k <= 64; ++k)  // C(64,32) ~ 1.8e18 fits; recurrence avoids overflow
+        tab[n][k] = k > n ? 0 : (k == 0 || k == n) ? 1 : tab[n - 1][k - 1] + tab[n - 1][k];
+    MIHG_CUDA(cudaMalloc(reinterpret_cast<void**>(&per_device[dev]), sizeof(tab)));
+    MIHG_CUDA(cudaMemcpy(per_device[dev], tab, sizeof(tab), cudaMemcpyHostToDevice));
+  }
+  return per_device[dev];
 }
 
 static std::atomic<uint64_t> g_launches{0};
@@ -295,6 +302,7 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
   MIHG_CUDA(cudaStreamSynchronize(st));
   t->non_empty_buckets = hs[0];
   t->max_bucket = hs[1];
+  t->non_empty_groups = hs[2];
   if (dense && nb < 32) {  // tiny table: stats on the host
     std::vector<uint32_t> off(nb + 1);
     MIHG_CUDA(cudaMemcpy(off.data(), t->offsets.get(), (nb + 1) * 4, cudaMemcpyDeviceToHost));
@@ -303,6 +311,7 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
       t->non_empty_buckets += c != 0;
       t->max_bucket = std::max<uint64_t>(t->max_bucket, c);
     }
+    t->non_empty_groups = t->non_empty_buckets ? 1 : 0;
   }
   idx.tables[j] = std::move(t);
 }
@@ -355,7 +364,7 @@ Index* build_index(const uint64_t* codes, bool codes_on_device, uint64_t n, uint
   idx->device = device;
   MIHG_CUDA(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));
   cudaStream_t st = idx->stream;
-  upload_binomials();
+  device_binomials();
   idx->bits = bits;
   idx->W = words_per_code(bits);
   idx->m = m;

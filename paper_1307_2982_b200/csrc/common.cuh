@@ -80,9 +80,10 @@ struct DevSubstring {
   uint32_t pos_base;  // index into positions[] otherwise
 };
 
-// Binomial coefficients C(n, k) for n, k <= 64 (ring sizes, colex unranking).
-extern __constant__ uint64_t c_binom[65][65];
-void upload_binomials();
+// Binomial coefficients C(n, k) for n, k <= 64 (ring sizes, colex unranking), in global memory:
+// lanes index it divergently, which constant memory would serialise.
+constexpr int kBinomStride = 65;
+const uint64_t* device_binomials();  // [65][65] on the current device
 uint64_t host_binom(uint32_t n, uint32_t k);
 
 // ---- bucket probe: [lo, hi) slice of ids[] for bucket `v` (table.hpp:178-188 semantics).

@@ -20,6 +20,7 @@ struct TableStorage {
   DeviceBuffer<uint64_t> tcodes;   // optional: codes in table order (bucket = contiguous run)
   uint64_t escaped_blocks = 0;
   uint64_t non_empty_buckets = 0;
+  uint64_t non_empty_groups = 0;  // 32-bucket groups (the reference's accounting unit)
   uint64_t max_bucket = 0;
   DevTable view() const {
     return DevTable{ids.get(), offsets.get(), dir.get(), esc.get(), tcodes.get(), s, dense ? 1u : 0u};

@@ -23,6 +23,7 @@
 //    buffer overflowed with a relevant key re-run their steps with the final radius as the bound
 //    into exactly-sized buffers.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "knn.cuh"
@@ -81,14 +82,16 @@ Index::~Index() {
 namespace {
 
 // colex unranking: the idx-th z-subset of {0..s-1} (Gosper order) as a bit mask.
-__device__ __forceinline__ uint64_t unrank_comb(uint64_t idx, uint32_t s, uint32_t z) {
+__device__ __forceinline__ uint64_t unrank_comb(const uint64_t* __restrict__ binom, uint64_t idx,
+                                                uint32_t s, uint32_t z) {
   uint64_t mask = 0;
   uint32_t c = s;
   for (uint32_t t = z; t >= 1; --t) {
     uint32_t cc = c - 1;
-    while (c_binom[cc][t] > idx) --cc;
+    uint64_t b = __ldg(binom + cc * kBinomStride + t);
+    while (b > idx) b = __ldg(binom + (--cc) * kBinomStride + t);
     mask |= uint64_t(1) << cc;
-    idx -= c_binom[cc][t];
+    idx -= b;
     c = cc;
   }
   return mask;
@@ -196,6 +199,7 @@ struct ProbeArgs {
   Piece* pieces;            // nullable: no piece queue
   uint32_t* piece_count;
   uint32_t piece_cap;
+  const uint64_t* binom;    // device_binomials()
 };
 
 // Is step (a, rr) the first step that reaches a candidate whose substring distances are d_j?
@@ -226,43 +230,82 @@ __device__ __forceinline__ QueryCtx query_ctx(const ProbeArgs& p, uint32_t q) {
   return c;
 }
 
-// Verify table entry e (index.hpp:219-230): dedup by first discovery, full distance, and keep it
-// if it can still be among the k nearest (d <= U). With inline codes only the code is read; the
-// id is fetched for keepers only.
+// Verify up to two table entries per lane (index.hpp:219-230): dedup by first discovery, full
+// distance, keep if d <= U. All 32 lanes call it together (warp-uniform query, `valid` masks
+// lanes without an entry); keepers are appended with ONE atomic per warp and histogrammed with
+// one atomic per distinct distance. With inline codes the id is fetched for keepers only.
 template <int W>
-__device__ __forceinline__ void process_entry(const ProbeArgs& p, const QueryCtx& c, uint32_t e,
-                                              const uint64_t* qc, uint32_t nw, uint64_t& n_new) {
-  Diff<W> df;
-  uint32_t id = 0;
+__device__ __forceinline__ void verify_entries(const ProbeArgs& p, const QueryCtx& c, bool v0,
+                                               uint32_t e0, bool v1, uint32_t e1, const uint64_t* qc,
+                                               uint32_t nw, uint64_t& n_new) {
+  Diff<W> d0, d1;
+  uint32_t id0 = 0, id1 = 0;
   if (p.tab.codes) {
-    df.load(p.tab.codes, e, qc, nw);
+    if (v0) d0.load(p.tab.codes, e0, qc, nw);
+    if (v1) d1.load(p.tab.codes, e1, qc, nw);
   } else {
-    id = __ldg(p.tab.ids + e);
-    df.load(p.codes, id, qc, nw);
+    if (v0) id0 = __ldg(p.tab.ids + e0);
+    if (v1) id1 = __ldg(p.tab.ids + e1);
+    if (v0) d0.load(p.codes, id0, qc, nw);
+    if (v1) d1.load(p.codes, id1, qc, nw);
   }
-  if (!first_discovery<W>(df, p)) return;
-  ++n_new;
-  const uint32_t d = df.dist(nw);
-  if (d > c.U) return;
-  if (p.tab.codes) id = __ldg(p.tab.ids + e);
-  if (p.hist) atomicAdd(p.hist + uint64_t(c.q) * p.b1 + d, 1u);
-  const uint32_t pos = atomicAdd(p.bufcnt + c.q, 1u);
-  if (pos < c.cap) p.buf[c.base + pos] = (uint64_t(d) << 32) | id;
-  else atomicMin(p.dropmin + c.q, d);
+  bool k0 = false, k1 = false;
+  uint32_t dist0 = 0, dist1 = 0;
+  if (v0 && first_discovery<W>(d0, p)) {
+    ++n_new;
+    dist0 = d0.dist(nw);
+    k0 = dist0 <= c.U;
+  }
+  if (v1 && first_discovery<W>(d1, p)) {
+    ++n_new;
+    dist1 = d1.dist(nw);
+    k1 = dist1 <= c.U;
+  }
+  const uint32_t b0 = __ballot_sync(~0u, k0), b1 = __ballot_sync(~0u, k1);
+  if ((b0 | b1) == 0) return;
+  if (p.tab.codes) {
+    if (k0) id0 = __ldg(p.tab.ids + e0);
+    if (k1) id1 = __ldg(p.tab.ids + e1);
+  }
+  const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
+  const uint32_t n0 = __popc(b0), total = n0 + __popc(b1);
+  uint32_t base = 0;
+  if (lane == 0) base = atomicAdd(p.bufcnt + c.q, total);
+  base = __shfl_sync(~0u, base, 0);
+  if (p.hist) {
+    const uint32_t key0 = k0 ? dist0 : 0xFFFFFFFFu, key1 = k1 ? dist1 : 0xFFFFFFFEu;
+    const uint32_t m0 = __match_any_sync(~0u, key0);
+    if (k0 && (m0 & lt) == 0) atomicAdd(p.hist + uint64_t(c.q) * p.b1 + dist0, __popc(m0));
+    const uint32_t m1 = __match_any_sync(~0u, key1);
+    if (k1 && (m1 & lt) == 0) atomicAdd(p.hist + uint64_t(c.q) * p.b1 + dist1, __popc(m1));
+  }
+  if (k0) {
+    const uint32_t pos = base + __popc(b0 & lt);
+    if (pos < c.cap) p.buf[c.base + pos] = (uint64_t(dist0) << 32) | id0;
+    else atomicMin(p.dropmin + c.q, dist0);
+  }
+  if (k1) {
+    const uint32_t pos = base + n0 + __popc(b1 & lt);
+    if (pos < c.cap) p.buf[c.base + pos] = (uint64_t(dist1) << 32) | id1;
+    else atomicMin(p.dropmin + c.q, dist1);
+  }
 }
 
 constexpr int kProbeThreads = 256;
 constexpr int kProbeWarps = kProbeThreads / 32;
 
 // Warp-cooperative MIH step. A work unit is (active query, warp chunk of 32*chunk ring indices);
-// lane l walks its own `chunk` consecutive ring indices. Per iteration every lane probes one
-// bucket, the warp prefix-sums the bucket sizes and then verifies the union of the entries
-// lane-parallel (entry t belongs to the lane whose [off, off + cnt) holds t), so skew between
-// buckets never idles the warp. Buckets above kInlineMax go to the piece queue.
-template <int W, bool kTrace>
+// lane l walks its own `chunk` consecutive ring indices, kLaneProbes per iteration (independent
+// directory loads in flight). The warp prefix-sums the 128 bucket sizes and verifies the union
+// of the entries lane-parallel, two per lane per pass (entry t belongs to the bucket whose
+// [off, off + cnt) holds t: 7-step binary search in shared memory), so bucket-size skew never
+// idles the warp. Buckets above kInlineMax go to the piece queue.
+template <int W, bool kTrace, int kLaneProbes>
 __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
-  __shared__ uint32_t s_lo[kProbeWarps][32];
-  __shared__ uint32_t s_off[kProbeWarps][33];
+  constexpr int kWarpBuckets = 32 * kLaneProbes;
+  constexpr int kSearchSteps = kLaneProbes == 1 ? 5 : kLaneProbes == 2 ? 6 : 7;
+  __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
+  __shared__ uint32_t s_off[kProbeWarps][kWarpBuckets];
   const uint32_t nw = W ? W : p.nw;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t span = uint64_t(p.chunk) * 32;  // ring indices per warp unit
@@ -276,7 +319,7 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
     const uint64_t uend = min(p.ring, ubeg + span);
     uint64_t i = ubeg + uint64_t(lane) * p.chunk;
     const uint64_t iend = min(uend, i + p.chunk);
-    uint64_t mask = i < iend ? unrank_comb(i, p.tab.s, p.rr) : 0;
+    uint64_t mask = i < iend ? unrank_comb(p.binom, i, p.tab.s, p.rr) : 0;
     const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
     uint64_t qreg[W ? W : 1];
     const uint64_t* qptr = p.qcodes + uint64_t(q) * nw;
@@ -287,27 +330,38 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
     const uint64_t* qc = W ? qreg : qptr;
     const QueryCtx ctx = query_ctx(p, q);
     uint64_t n_cand = 0, n_new = 0;
-    for (uint32_t it = 0; it < p.chunk; ++it, ++i) {
-      uint32_t lo = 0, hi = 0;
-      if (i < iend) {
-        probe_bucket(p.tab, qa ^ uint32_t(mask), lo, hi);
-        mask = next_comb(mask);
-      }
-      uint32_t cnt = hi - lo;
-      n_cand += cnt;
-      if (cnt > kInlineMax && p.pieces) {
-        const uint32_t np = (cnt + kPieceSize - 1) / kPieceSize;
-        const uint32_t at = atomicAdd(p.piece_count, np);
-        if (at + np <= p.piece_cap) {
-          for (uint32_t t = 0; t < np; ++t)
-            p.pieces[at + t] = Piece{q, lo + t * kPieceSize, min(kPieceSize, cnt - t * kPieceSize), 0};
-          cnt = 0;
-        } else {
-          for (uint32_t t = at; t < p.piece_cap && t < at + np; ++t) p.pieces[t] = Piece{q, 0, 0, 0};
+    for (uint32_t it = 0; it < p.chunk; it += kLaneProbes) {
+      uint32_t lo[kLaneProbes], cnt[kLaneProbes];
+#pragma unroll
+      for (int b = 0; b < kLaneProbes; ++b) {
+        uint32_t l = 0, h = 0;
+        if (i < iend && it + b < p.chunk) {
+          probe_bucket(p.tab, qa ^ uint32_t(mask), l, h);
+          mask = next_comb(mask);
+          ++i;
         }
+        lo[b] = l;
+        cnt[b] = h - l;
       }
-      // warp exclusive prefix of the bucket sizes
-      uint32_t incl = cnt;
+      uint32_t mine = 0;
+#pragma unroll
+      for (int b = 0; b < kLaneProbes; ++b) {
+        n_cand += cnt[b];
+        if (cnt[b] > kInlineMax && p.pieces) {
+          const uint32_t np = (cnt[b] + kPieceSize - 1) / kPieceSize;
+          const uint32_t at = atomicAdd(p.piece_count, np);
+          if (at + np <= p.piece_cap) {
+            for (uint32_t t = 0; t < np; ++t)
+              p.pieces[at + t] = Piece{q, lo[b] + t * kPieceSize, min(kPieceSize, cnt[b] - t * kPieceSize), 0};
+            cnt[b] = 0;
+          } else {
+            for (uint32_t t = at; t < p.piece_cap && t < at + np; ++t) p.pieces[t] = Piece{q, 0, 0, 0};
+          }
+        }
+        mine += cnt[b];
+      }
+      // warp exclusive prefix of the per-lane totals; buckets laid out lane-major
+      uint32_t incl = mine;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(~0u, incl, o);
@@ -315,19 +369,32 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
       }
       const uint32_t total = __shfl_sync(~0u, incl, 31);
       if (total == 0) continue;
-      s_lo[wib][lane] = lo;
-      s_off[wib][lane] = incl - cnt;
-      __syncwarp();
-      for (uint32_t t = lane; t < total; t += 32) {
-        // owner lane: last l with off[l] <= t (binary search over the 32 offsets)
-        uint32_t lo_l = 0, hi_l = 32;
+      uint32_t off = incl - mine;
 #pragma unroll
-        for (int step = 0; step < 5; ++step) {
-          const uint32_t mid = (lo_l + hi_l) >> 1;
-          if (s_off[wib][mid] <= t) lo_l = mid;
-          else hi_l = mid;
+      for (int b = 0; b < kLaneProbes; ++b) {
+        s_lo[wib][lane * kLaneProbes + b] = lo[b];
+        s_off[wib][lane * kLaneProbes + b] = off;
+        off += cnt[b];
+      }
+      __syncwarp();
+      for (uint32_t t0 = 0; t0 < total; t0 += 64) {
+        uint32_t e[2];
+        bool v[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t t = t0 + h * 32 + lane;
+          v[h] = t < total;
+          // owning bucket: last slot with off <= t (binary search over 128 offsets)
+          uint32_t a = 0, bnd = kWarpBuckets;
+#pragma unroll
+          for (int step = 0; step < kSearchSteps; ++step) {
+            const uint32_t mid = (a + bnd) >> 1;
+            if (s_off[wib][mid] <= t) a = mid;
+            else bnd = mid;
+          }
+          e[h] = s_lo[wib][a] + (t - s_off[wib][a]);
         }
-        process_entry<W>(p, ctx, s_lo[wib][lo_l] + (t - s_off[wib][lo_l]), qc, nw, n_new);
+        verify_entries<W>(p, ctx, v[0], e[0], v[1], e[1], qc, nw, n_new);
       }
       __syncwarp();
     }
@@ -345,7 +412,7 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
   }
 }
 
-// One warp per queued piece of a big bucket.
+// One warp per queued piece of a big bucket (64 entries per pass).
 template <int W, bool kTrace>
 __global__ void __launch_bounds__(kProbeThreads) mih_piece_kernel(ProbeArgs p) {
   const uint32_t nw = W ? W : p.nw;
@@ -364,7 +431,9 @@ __global__ void __launch_bounds__(kProbeThreads) mih_piece_kernel(ProbeArgs p) {
     const uint64_t* qc = W ? qreg : qptr;
     const QueryCtx ctx = query_ctx(p, pc.q);
     uint64_t n_new = 0;
-    for (uint32_t t = lane; t < pc.cnt; t += 32) process_entry<W>(p, ctx, pc.lo + t, qc, nw, n_new);
+    for (uint32_t t0 = 0; t0 < pc.cnt; t0 += 64)
+      verify_entries<W>(p, ctx, t0 + lane < pc.cnt, pc.lo + t0 + lane, t0 + 32 + lane < pc.cnt,
+                        pc.lo + t0 + 32 + lane, qc, nw, n_new);
     if (kTrace) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) n_new += __shfl_xor_sync(~0u, n_new, o);
@@ -482,13 +551,26 @@ __global__ void zero_trace_kernel(uint64_t nq, Trace* traces) {
     traces[q] = Trace{0, 0, 0, 0, 0, 0};
 }
 
+// Buckets probed per lane per iteration (MIHG_LANE_PROBES=1|2|4; default 2).
+int lane_probes() {
+  static const int v = [] {
+    const char* e = std::getenv("MIHG_LANE_PROBES");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
+}
+
 template <int W, bool kTrace>
 void launch_probe(const ProbeArgs& p, cudaStream_t st) {
   const uint64_t blocks_needed = (p.total + kProbeWarps - 1) / kProbeWarps;
   const uint64_t max_blocks = uint64_t(device_sm_count()) * 8;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
   if (p.pieces) MIHG_CUDA(cudaMemsetAsync(p.piece_count, 0, 4, st));
-  mih_probe_kernel<W, kTrace><<<grid, kProbeThreads, 0, st>>>(p);
+  switch (lane_probes()) {
+    case 1: mih_probe_kernel<W, kTrace, 1><<<grid, kProbeThreads, 0, st>>>(p); break;
+    case 4: mih_probe_kernel<W, kTrace, 4><<<grid, kProbeThreads, 0, st>>>(p); break;
+    default: mih_probe_kernel<W, kTrace, 2><<<grid, kProbeThreads, 0, st>>>(p);
+  }
   MIHG_LAUNCH();
   if (p.pieces) {
     mih_piece_kernel<W, kTrace><<<unsigned(max_blocks), kProbeThreads, 0, st>>>(p);
@@ -593,6 +675,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   p.pieces = ws.pieces.get();
   p.piece_count = ws.piece_count.get();
   p.piece_cap = kPieceQueue;
+  p.binom = device_binomials();
 
   std::vector<uint64_t> lookups_prefix;
   uint32_t* act_in = ws.act0.get();

@@ -168,6 +168,23 @@ def main():
                                ids=np.concatenate(recs_ids).astype(np.uint32),
                                offs=np.array(recs_off, np.uint64))
 
+    # TableStats (table.hpp:190-197) of every table: non_empty_buckets, max_bucket_size,
+    # total_entries, estimated_bytes.
+    import ctypes as C
+    stats = {}
+    for name, n, bits, seed, m in (("b64m4", 1200, 64, 175, 4), ("b64m3", 20000, 64, 777, 3),
+                                   ("b100m8", 800, 100, 60, 8), ("b64m2", 50000, 64, 31, 2)):
+        codes = R.gen_uniform(n, bits, seed)
+        h = R.build(codes, bits, m)
+        rows = []
+        for j in range(m):
+            out = np.zeros(4, np.uint64)
+            assert R.lib.ref_table_stats(h.h, j, out.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
+            rows.append(out)
+        stats[name] = np.stack(rows)
+        stats[name + "_spec"] = np.array([n, bits, seed, m], np.uint64)
+    files["table_stats"] = stats
+
     # gen_uniform pins (io.hpp:266-277): several widths and seeds.
     pins = {}
     for n, bits, seed in ((5, 64, 1), (7, 70, 181), (3, 256, 42), (4, 24, 501), (2, 130, 9)):

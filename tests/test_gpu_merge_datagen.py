@@ -11,7 +11,7 @@ def test_merge_topk_matches_numpy(cuda_ok):
     import torch
 
     from paper_1307_2982_b200.shard import gpu_merge
-    from tests.test_shard_gloo import numpy_merge
+    from _helpers import numpy_merge
 
     rng = np.random.default_rng(3)
     for G, nq, k_in, k in ((2, 50, 10, 10), (8, 300, 100, 100), (4, 7, 5, 17), (3, 20, 64, 1)):

@@ -228,3 +228,21 @@ def test_random_shapes_vs_oracle(cuda_ok, port, bits, m, n):
             t = _trace_array(tr)
             assert np.array_equal(t[:, 4], od[:, -1]), "final_radius == d_k"
             assert np.array_equal(t, closed_form_traces(db.raw_words(), bits, m, qs, t[:, 4])), (layout, k)
+
+
+@pytest.mark.parametrize("layout", ["auto", "sparse"])
+def test_table_stats_match_reference(cuda_ok, golden, layout):
+    # TableStats (table.hpp:33-47, :190-197): non_empty_buckets, max_bucket_size, total_entries,
+    # estimated_bytes (the reference's accounting model) for every table
+    mg = _mg()
+    d = golden("table_stats")
+    for name in [k for k in d if not k.endswith("_spec")]:
+        n, bits, seed, m = (int(x) for x in d[name + "_spec"])
+        if layout == "sparse" and (bits // m) < 6:
+            continue
+        db = mg.gen_uniform(n, bits, seed)
+        idx = mg.MihIndex.build(db, mg.consecutive_partition(bits, m), layout=layout)
+        for j in range(m):
+            st = idx.table(j).stats()
+            got = [st.non_empty_buckets, st.max_bucket_size, st.total_entries, st.estimated_bytes]
+            assert got == [int(x) for x in d[name][j]], (name, j)

@@ -13,6 +13,8 @@ import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
+from _helpers import numpy_merge  # noqa: E402
+
 
 def _free_port():
     s = socket.socket()
@@ -22,21 +24,11 @@ def _free_port():
     return p
 
 
-def numpy_merge(all_ids, all_d, k):
-    """Smallest k packed keys (dist << 32 | id) per query; padding dist 0xFFFFFFFF sorts last."""
-    ids = all_ids.numpy().view(np.uint32).astype(np.uint64)
-    d = all_d.numpy().view(np.uint32).astype(np.uint64)
-    keys = (d << np.uint64(32)) | ids  # [G, nq, k]
-    keys = np.sort(np.concatenate(list(keys), axis=1), axis=1)[:, :k]
-    out_d = (keys >> np.uint64(32)).astype(np.uint32)
-    out_i = (keys & np.uint64(0xFFFFFFFF)).astype(np.uint32)
-    return torch.from_numpy(out_i.view(np.int32)), torch.from_numpy(out_d.view(np.int32))
-
-
 def _worker(rank, world, port, n, bits, m, k, result_q):
     import sys
 
     sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)

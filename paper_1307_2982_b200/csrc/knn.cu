@@ -234,7 +234,7 @@ __device__ __forceinline__ QueryCtx query_ctx(const ProbeArgs& p, uint32_t q) {
 // distance, keep if d <= U. All 32 lanes call it together (warp-uniform query, `valid` masks
 // lanes without an entry); keepers are appended with ONE atomic per warp and histogrammed with
 // one atomic per distinct distance. With inline codes the id is fetched for keepers only.
-template <int W>
+template <int W, bool kTrace>
 __device__ __forceinline__ void verify_entries(const ProbeArgs& p, const QueryCtx& c, bool v0,
                                                uint32_t e0, bool v1, uint32_t e1, const uint64_t* qc,
                                                uint32_t nw, uint64_t& n_new) {
@@ -249,17 +249,16 @@ __device__ __forceinline__ void verify_entries(const ProbeArgs& p, const QueryCt
     if (v0) d0.load(p.codes, id0, qc, nw);
     if (v1) d1.load(p.codes, id1, qc, nw);
   }
-  bool k0 = false, k1 = false;
-  uint32_t dist0 = 0, dist1 = 0;
-  if (v0 && first_discovery<W>(d0, p)) {
-    ++n_new;
-    dist0 = d0.dist(nw);
-    k0 = dist0 <= c.U;
-  }
-  if (v1 && first_discovery<W>(d1, p)) {
-    ++n_new;
-    dist1 = d1.dist(nw);
-    k1 = dist1 <= c.U;
+  const uint32_t dist0 = v0 ? d0.dist(nw) : 0u, dist1 = v1 ? d1.dist(nw) : 0u;
+  bool k0, k1;
+  if constexpr (kTrace) {  // unique_candidates counts every first discovery
+    const bool f0 = v0 && first_discovery<W>(d0, p), f1 = v1 && first_discovery<W>(d1, p);
+    n_new += uint64_t(f0) + uint64_t(f1);
+    k0 = f0 && dist0 <= c.U;
+    k1 = f1 && dist1 <= c.U;
+  } else {  // only keepers matter: bound first, dedup second
+    k0 = v0 && dist0 <= c.U && first_discovery<W>(d0, p);
+    k1 = v1 && dist1 <= c.U && first_discovery<W>(d1, p);
   }
   const uint32_t b0 = __ballot_sync(~0u, k0), b1 = __ballot_sync(~0u, k1);
   if ((b0 | b1) == 0) return;
@@ -301,7 +300,7 @@ constexpr int kProbeWarps = kProbeThreads / 32;
 // [off, off + cnt) holds t: 7-step binary search in shared memory), so bucket-size skew never
 // idles the warp. Buckets above kInlineMax go to the piece queue.
 template <int W, bool kTrace, int kLaneProbes>
-__global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
+__global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kernel(ProbeArgs p) {
   constexpr int kWarpBuckets = 32 * kLaneProbes;
   constexpr int kSearchSteps = kLaneProbes == 1 ? 5 : kLaneProbes == 2 ? 6 : 7;
   __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
@@ -394,7 +393,7 @@ __global__ void __launch_bounds__(kProbeThreads) mih_probe_kernel(ProbeArgs p) {
           }
           e[h] = s_lo[wib][a] + (t - s_off[wib][a]);
         }
-        verify_entries<W>(p, ctx, v[0], e[0], v[1], e[1], qc, nw, n_new);
+        verify_entries<W, kTrace>(p, ctx, v[0], e[0], v[1], e[1], qc, nw, n_new);
       }
       __syncwarp();
     }
@@ -432,7 +431,7 @@ __global__ void __launch_bounds__(kProbeThreads) mih_piece_kernel(ProbeArgs p) {
     const QueryCtx ctx = query_ctx(p, pc.q);
     uint64_t n_new = 0;
     for (uint32_t t0 = 0; t0 < pc.cnt; t0 += 64)
-      verify_entries<W>(p, ctx, t0 + lane < pc.cnt, pc.lo + t0 + lane, t0 + 32 + lane < pc.cnt,
+      verify_entries<W, kTrace>(p, ctx, t0 + lane < pc.cnt, pc.lo + t0 + lane, t0 + 32 + lane < pc.cnt,
                         pc.lo + t0 + 32 + lane, qc, nw, n_new);
     if (kTrace) {
 #pragma unroll

@@ -23,6 +23,7 @@
 //    buffer overflowed with a relevant key re-run their steps with the final radius as the bound
 //    into exactly-sized buffers.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 
@@ -46,6 +47,8 @@ struct Workspace {
   DeviceBuffer<uint64_t> lookups_prefix;
   DeviceBuffer<Piece> pieces;
   DeviceBuffer<uint32_t> piece_count;
+  DeviceBuffer<uint64_t> slice_cnt, slice_prefix, work_total;
+  DeviceBuffer<unsigned long long> work_counter;
   uint32_t* h_counter = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -200,7 +203,37 @@ struct ProbeArgs {
   uint32_t* piece_count;
   uint32_t piece_cap;
   const uint64_t* binom;    // device_binomials()
+  // L2-sliced rounds (slice_bits > 0): units enumerated per (slice P, active slot), P-major
+  uint32_t slice_bits;
+  uint64_t nact, npairs;
+  const uint64_t* unit_prefix;  // exclusive prefix of units per pair (npairs)
+  const uint64_t* work_total;   // total units (device)
+  unsigned long long* work_counter;
 };
+
+// Units per (slice P, active slot) of a sliced round: the ring's sub-ring inside slice P has
+// the top flip pattern T = P ^ (q_a >> s') fixed and rr - popc(T) flips in the low s' bits.
+__global__ void slice_units_kernel(ProbeArgs p, uint64_t span, uint64_t* __restrict__ cnt) {
+  const uint32_t sb = p.tab.s - p.slice_bits;
+  for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < p.npairs;
+       idx += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t P = uint32_t(idx / p.nact);
+    const uint64_t slot = idx - uint64_t(P) * p.nact;
+    const uint32_t q = p.active[slot];
+    uint64_t c = 0;
+    if (!(p.rlimit && p.r > p.rlimit[q])) {
+      const uint32_t h = __popc(P ^ (p.qsub[uint64_t(q) * p.m + p.a] >> sb));
+      if (h <= p.rr && p.rr - h <= sb) c = (p.binom[sb * kBinomStride + (p.rr - h)] + span - 1) / span;
+    }
+    cnt[idx] = c;
+  }
+}
+
+__global__ void slice_total_kernel(const uint64_t* __restrict__ prefix, const uint64_t* __restrict__ cnt,
+                                   uint64_t npairs, uint64_t* total, unsigned long long* counter) {
+  *total = prefix[npairs - 1] + cnt[npairs - 1];
+  *counter = 0;
+}
 
 // Is step (a, rr) the first step that reaches a candidate whose substring distances are d_j?
 // New iff for j < a: d_j > rr, and for j > a: d_j >= rr (r == min_j m*d_j + j).
@@ -309,16 +342,43 @@ __global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kerne
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t span = uint64_t(p.chunk) * 32;  // ring indices per warp unit
   const uint64_t nwarps = uint64_t(gridDim.x) * kProbeWarps;
-  for (uint64_t u = blockIdx.x * uint64_t(kProbeWarps) + wib; u < p.total; u += nwarps) {
-    const uint64_t slot = u / p.cpq;
-    const uint64_t part = u - slot * p.cpq;
+  uint64_t u = blockIdx.x * uint64_t(kProbeWarps) + wib;
+  for (;; u += nwarps) {
+    uint64_t slot, part, ring = p.ring, high = 0;
+    uint32_t zbits = p.rr, sbits = p.tab.s;
+    if (p.slice_bits) {
+      // sliced round: units are claimed in order (slice-major), so the warps in flight probe
+      // one L2-sized slice of the table at a time
+      if (lane == 0) u = atomicAdd(p.work_counter, 1ull);
+      u = __shfl_sync(~0u, u, 0);
+      if (u >= *p.work_total) break;
+      uint64_t lo_i = 0, hi_i = p.npairs;  // last pair with prefix <= u
+      while (hi_i - lo_i > 1) {
+        const uint64_t mid = (lo_i + hi_i) >> 1;
+        if (__ldg(p.unit_prefix + mid) <= u) lo_i = mid;
+        else hi_i = mid;
+      }
+      const uint32_t P = uint32_t(lo_i / p.nact);
+      slot = lo_i - uint64_t(P) * p.nact;
+      part = u - __ldg(p.unit_prefix + lo_i);
+      sbits = p.tab.s - p.slice_bits;
+      const uint32_t qa0 = p.qsub[uint64_t(p.active[slot]) * p.m + p.a];
+      const uint32_t T = P ^ (qa0 >> sbits);  // flip pattern of the top slice bits
+      zbits = p.rr - __popc(T);               // count kernel guarantees 0 <= zbits <= sbits
+      ring = __ldg(p.binom + sbits * kBinomStride + zbits);
+      high = uint64_t(T) << sbits;
+    } else {
+      if (u >= p.total) break;
+      slot = u / p.cpq;
+      part = u - slot * p.cpq;
+    }
     const uint32_t q = p.active[slot];
     if (p.rlimit && p.r > p.rlimit[q]) continue;
     const uint64_t ubeg = part * span;
-    const uint64_t uend = min(p.ring, ubeg + span);
+    const uint64_t uend = min(ring, ubeg + span);
     uint64_t i = ubeg + uint64_t(lane) * p.chunk;
     const uint64_t iend = min(uend, i + p.chunk);
-    uint64_t mask = i < iend ? unrank_comb(p.binom, i, p.tab.s, p.rr) : 0;
+    uint64_t mask = i < iend ? unrank_comb(p.binom, i, sbits, zbits) : 0;
     const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
     uint64_t qreg[W ? W : 1];
     const uint64_t* qptr = p.qcodes + uint64_t(q) * nw;
@@ -335,7 +395,7 @@ __global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kerne
       for (int b = 0; b < kLaneProbes; ++b) {
         uint32_t l = 0, h = 0;
         if (i < iend && it + b < p.chunk) {
-          probe_bucket(p.tab, qa ^ uint32_t(mask), l, h);
+          probe_bucket(p.tab, qa ^ uint32_t(high | mask), l, h);
           mask = next_comb(mask);
           ++i;
         }
@@ -563,7 +623,8 @@ template <int W, bool kTrace>
 void launch_probe(const ProbeArgs& p, cudaStream_t st) {
   const uint64_t blocks_needed = (p.total + kProbeWarps - 1) / kProbeWarps;
   const uint64_t max_blocks = uint64_t(device_sm_count()) * 8;
-  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
+  const unsigned grid = p.slice_bits ? unsigned(max_blocks)
+                                     : unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
   if (p.pieces) MIHG_CUDA(cudaMemsetAsync(p.piece_count, 0, 4, st));
   switch (lane_probes()) {
     case 1: mih_probe_kernel<W, kTrace, 1><<<grid, kProbeThreads, 0, st>>>(p); break;
@@ -605,6 +666,54 @@ void plan_round(ProbeArgs& p, uint64_t nact) {
   p.total = nact * p.cpq;
 }
 
+// L2-sliced probing for tables whose probe structure exceeds L2 (north_star: the 32-bit sparse
+// tables): pick t so one slice of the directory/offsets is <= 32 MB, for rounds large enough
+// (>= 4M probes) to amortise the per-(slice, query) unit table. Experimental, off by default
+// (MIHG_SLICE=1 enables): measured slower on config 4 (unit decode cost).
+bool slicing_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MIHG_SLICE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+void plan_slicing(ProbeArgs& p, Workspace& ws, uint64_t nact, cudaStream_t st) {
+  p.slice_bits = 0;
+  const uint32_t s = p.tab.s;
+  const double bytes = p.tab.dense ? double((uint64_t(1) << s) + 1) * 4
+                                   : double(uint64_t(1) << (s - kDirBucketsLog2)) * sizeof(DirBlock);
+  if (!slicing_enabled() || bytes <= 64.0 * (1 << 20) || double(nact) * double(p.ring) < 4.0e6) return;
+  uint32_t t = 0;
+  while (bytes / double(1u << t) > 32.0 * (1 << 20) && t < 12) ++t;
+  t = std::min<uint32_t>(t, s - 1);
+  while (t > 0 && (uint64_t(nact) << t) > (uint64_t(1) << 23)) --t;  // bound the unit table
+  if (t == 0) return;
+  const uint64_t npairs = uint64_t(nact) << t;
+  if (ws.slice_cnt.size() < npairs) {
+    ws.slice_cnt = DeviceBuffer<uint64_t>(npairs, st);
+    ws.slice_prefix = DeviceBuffer<uint64_t>(npairs, st);
+  }
+  // Keep the in-flight wavefront inside one slice: units per slice >= 4x the resident warps.
+  const double resident_warps = double(device_sm_count()) * 64;
+  const double lanes_per_slice = double(nact) * double(p.ring) / double(1u << t);
+  const double chunk = std::floor(lanes_per_slice / (4.0 * resident_warps * 32.0));
+  p.chunk = uint32_t(std::max(1.0, std::min(chunk, 256.0)));
+  p.slice_bits = t;
+  p.nact = nact;
+  p.npairs = npairs;
+  p.unit_prefix = ws.slice_prefix.get();
+  p.work_total = ws.work_total.get();
+  p.work_counter = ws.work_counter.get();
+  const uint64_t span = uint64_t(p.chunk) * 32;
+  slice_units_kernel<<<unsigned(std::min<uint64_t>((npairs + 255) / 256, 8192)), 256, 0, st>>>(p, span, ws.slice_cnt.get());
+  MIHG_LAUNCH();
+  exclusive_scan<uint64_t>(ws.slice_cnt.get(), ws.slice_prefix.get(), npairs, st);
+  slice_total_kernel<<<1, 1, 0, st>>>(ws.slice_prefix.get(), ws.slice_cnt.get(), npairs, ws.work_total.get(),
+                                      ws.work_counter.get());
+  MIHG_LAUNCH();
+}
+
 constexpr uint32_t kPieceQueue = 1u << 24;  // 16M pieces (256 MB); overflow falls back inline
 
 void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
@@ -632,6 +741,8 @@ void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
   ws->lookups_prefix = DeviceBuffer<uint64_t>(b1 + 1, st);
   ws->pieces = DeviceBuffer<Piece>(kPieceQueue, st);
   ws->piece_count = DeviceBuffer<uint32_t>(1, st);
+  ws->work_total = DeviceBuffer<uint64_t>(1, st);
+  ws->work_counter = DeviceBuffer<unsigned long long>(1, st);
   MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_counter), 16));
   MIHG_CUDA(cudaEventCreate(&ws->ev0));
   MIHG_CUDA(cudaEventCreate(&ws->ev1));
@@ -696,6 +807,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
       p.active = act_in;
       p.ring = ring;
       plan_round(p, nact);
+      plan_slicing(p, ws, nact, st);
       ProfileState& prof = profile();
       if (prof.enabled) MIHG_CUDA(cudaEventRecord(ws.ev0, st));
       dispatch_probe(p, d_tr != nullptr, st);
@@ -782,6 +894,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     rp.r = r;
     rp.ring = ring;
     plan_round(rp, nre);
+    plan_slicing(rp, ws, nre, st);
     dispatch_probe(rp, false, st);
   }
   // select the re-run queries from their exact buffers

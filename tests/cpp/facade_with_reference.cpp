@@ -16,11 +16,13 @@
 
 int main() {
   int bad = 0;
+  // shapes whose reference CPU search is cheap (substrings <= 24 bits: 32-bit substrings at
+  // n = 2e4 put the reference in its exhaustive-probing regime, minutes per query)
   for (uint32_t bits : {64u, 70u, 128u}) {
     mih::CodeDatabase db = mih::gen_uniform(20000, bits, 900 + bits);
     mih::CodeDatabase qs = mih::gen_uniform(30, bits, 901 + bits);
     for (uint32_t m : {3u, 4u, 6u}) {
-      if ((bits + m - 1) / m > 32) continue;
+      if ((bits + m - 1) / m > 24) continue;
       mih::Partition p = mih::consecutive_partition(bits, m);
       mih::MihIndex cpu = mih::MihIndex::build(db, p);
       auto gpu = mihg::MihIndex<mih::Neighbor>::build(db, p);

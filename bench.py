@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=0, help="queries per CPU-reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--method", default="mih", choices=["mih", "scan"],
+                    help="mih: MihIndex::knn_search path (default); scan: the exhaustive K6 comparator")
     return ap.parse_args()
 
 
@@ -289,8 +291,12 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
-                              stream=stream.cuda_stream)
+        if args.method == "scan":
+            idx.scan_knn_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
+                                stream=stream.cuda_stream)
+        else:
+            idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
+                                  stream=stream.cuda_stream)
         if world > 1:
             dist.all_gather_into_tensor(all_ids, ids)
             dist.all_gather_into_tensor(all_d, dists)
@@ -353,16 +359,24 @@ def main():
     hd = torch.empty((nq, k), dtype=torch.int32).pin_memory()
     if world == 1:
         def e2e_step():
-            _lib.check(L.mihg_knn_batch(idx._h, C.cast(C.c_void_p(hq.data_ptr()), _lib.u64p), nq, k,
-                                        C.cast(C.c_void_p(hid.data_ptr()), _lib.u32p),
-                                        C.cast(C.c_void_p(hd.data_ptr()), _lib.u32p), None))
+            qp = C.cast(C.c_void_p(hq.data_ptr()), _lib.u64p)
+            ip = C.cast(C.c_void_p(hid.data_ptr()), _lib.u32p)
+            dp = C.cast(C.c_void_p(hd.data_ptr()), _lib.u32p)
+            if args.method == "scan":
+                _lib.check(L.mihg_scan_knn_batch(idx._h, qp, nq, k, ip, dp))
+            else:
+                _lib.check(L.mihg_knn_batch(idx._h, qp, nq, k, ip, dp, None))
     else:
         dq = torch.empty_like(queries)
 
         def e2e_step():
             dq.copy_(hq, non_blocking=True)
-            idx.knn_search_device(dq.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
-                                  stream=stream.cuda_stream)
+            if args.method == "scan":
+                idx.scan_knn_device(dq.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
+                                    stream=stream.cuda_stream)
+            else:
+                idx.knn_search_device(dq.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
+                                      stream=stream.cuda_stream)
             dist.all_gather_into_tensor(all_ids, ids)
             dist.all_gather_into_tensor(all_d, dists)
             _lib.check(L.mihg_merge_topk_device(C.c_void_p(all_ids.data_ptr()), C.c_void_p(all_d.data_ptr()),
@@ -396,15 +410,24 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else 0.0
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak if peak else None, "traffic": None,
-                "kernel": "mih_probe_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
-                "alg_bytes_per_step": alg_bytes, "probe_ms_per_step": probe_ms,
-                "probe_launches_per_step": probe_launches,
-                "step_frac_of_roofline": (alg_bytes / (ms_per_step / 1000.0) / 1e9) / peak,
-                "popc64_per_step": popc64,
-                "mean_trace": {"lookups": float(lookups.mean()), "candidates": float(cands.mean()),
-                               "unique": float(uniq.mean()), "final_radius": float(radius.mean())}}
+    if args.method == "scan":
+        # K6 is POPC-bound: n*W popc64 = 2*n*W POPC32 per query; peak = 16 POPC/clk/SM measured
+        # 4.56e12/s at 1.925 GHz (tools/probe/ubench.cu), scaled to the sampled SM clock.
+        pc_peak = 4.56e12 * ((clk.get("sm_mhz") or 1925.0) / 1925.0)
+        pc_ach = 2.0 * (hi - lo) * W * nq / (ms_per_step / 1000.0)
+        roofline = {"bound": "popc", "achieved": pc_ach / 1e12, "peak": pc_peak / 1e12, "unit": "TPOPC32/s",
+                    "frac": pc_ach / pc_peak, "traffic": None, "kernel": "scan_kernel",
+                    "peak_source": "tools/probe/ubench.cu POPC microbenchmark (16/clk/SM)"}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak if peak else None, "traffic": None,
+                    "kernel": "mih_probe_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+                    "alg_bytes_per_step": alg_bytes, "probe_ms_per_step": probe_ms,
+                    "probe_launches_per_step": probe_launches,
+                    "step_frac_of_roofline": (alg_bytes / (ms_per_step / 1000.0) / 1e9) / peak,
+                    "popc64_per_step": popc64,
+                    "mean_trace": {"lookups": float(lookups.mean()), "candidates": float(cands.mean()),
+                                   "unique": float(uniq.mean()), "final_radius": float(radius.mean())}}
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None

@@ -122,6 +122,16 @@ int mihg_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32
 int mihg_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
                           uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces, void* stream);
 
+/* MihIndex::range_search(BinaryCode q, uint32_t r, SearchTrace*, SearchScratch*) — index.hpp:149-176
+ * (paper Alg. 2), batched, host pointers. Every (id, dist) with dist <= r per query in (dist, id)
+ * order, query-major. out_offsets[nq+1] is always written (out_offsets[nq] = total); ids/dists
+ * (capacity entries each) are written only when total <= capacity — otherwise call again with
+ * larger buffers. r > bits -> MIHG_EINVAL. traces: nq or NULL (final_radius = 0 as the
+ * reference's range_search leaves it). */
+int mihg_range_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t r,
+                     uint64_t* out_offsets, uint32_t* out_ids, uint32_t* out_dists, uint64_t capacity,
+                     mihg_trace* traces);
+
 /* scan_knn(db, q, k) — scan.hpp:43-68, batched, over the index's device codes. */
 int mihg_scan_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,
                         uint32_t* out_ids, uint32_t* out_dists);

@@ -75,6 +75,8 @@ SYMBOLS = [
                                  C.POINTER(Trace)]),
     ("mihg_knn_batch_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
                                         C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mihg_range_batch", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint32, u64p, u32p, u32p,
+                                   C.c_uint64, C.POINTER(Trace)]),
     ("mihg_scan_knn_batch", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint32, u32p, u32p]),
     ("mihg_scan_knn_batch_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                              C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -257,6 +257,19 @@ int mihg_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32
   });
 }
 
+int mihg_range_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t r,
+                     uint64_t* out_offsets, uint32_t* out_ids, uint32_t* out_dists, uint64_t capacity,
+                     mihg_trace* traces) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    if (!out_offsets) throw mihg::InvalidArgument("range_search: null offsets");
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    mihg::range_host(ix, queries, nq, r, out_offsets, out_ids, out_dists, capacity,
+                     reinterpret_cast<mihg::Trace*>(traces), ix.stream);
+  });
+}
+
 int mihg_scan_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
                                uint32_t* d_ids, uint32_t* d_dists, void* stream) {
   return guarded([&] {

@@ -754,6 +754,95 @@ uint32_t read_counter(const uint32_t* d, uint32_t* h, cudaStream_t st) {
   return *h;
 }
 
+ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
+  ProbeArgs p{};
+  p.codes = idx.codes.get();
+  p.qcodes = d_q;
+  p.qsub = ws.qsub.get();
+  p.subs = idx.d_subs.get();
+  p.submask = idx.d_submask.get();
+  p.m = idx.m;
+  p.nw = idx.W;
+  p.hist = ws.hist.get();
+  p.b1 = idx.bits + 1;
+  p.ubound = ws.ubound.get();
+  p.buf = ws.buf.get();
+  p.cap_fixed = ws.cap;
+  p.bufcnt = ws.bufcnt.get();
+  p.dropmin = ws.dropmin.get();
+  p.trc = ws.trc.get();
+  p.pieces = ws.pieces.get();
+  p.piece_count = ws.piece_count.get();
+  p.piece_cap = kPieceQueue;
+  p.binom = device_binomials();
+  return p;
+}
+
+// Re-run of the queries whose bounded buffer dropped a key with dist <= final radius: their
+// steps 0..R are probed again with U = R into exactly-sized buffers (need = sum_{d<=R} hist),
+// without histogram or trace updates. Exact because first discovery is stateless.
+struct RerunResult {
+  std::vector<uint32_t> list, need, R;
+  std::vector<uint64_t> base;
+  DeviceBuffer<uint64_t> big;
+};
+
+RerunResult rerun_pass(Index& idx, const ProbeArgs& p, const uint32_t* d_rerun, uint32_t nre,
+                       const uint32_t* d_need, uint64_t nq, cudaStream_t st) {
+  Workspace& ws = *idx.ws;
+  const uint32_t m = idx.m;
+  RerunResult res;
+  res.list.resize(nre);
+  res.need.resize(nq);
+  res.R.resize(nq);
+  MIHG_CUDA(cudaMemcpyAsync(res.list.data(), d_rerun, nre * 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaMemcpyAsync(res.need.data(), d_need, nq * 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaMemcpyAsync(res.R.data(), ws.final_r.get(), nq * 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaStreamSynchronize(st));
+  std::sort(res.list.begin(), res.list.end());
+  res.base.assign(nq, 0);
+  std::vector<uint32_t> hcap(nq, 0);
+  uint64_t total = 0;
+  uint32_t maxR = 0;
+  for (uint32_t q : res.list) {
+    res.base[q] = total;
+    hcap[q] = res.need[q];
+    total += res.need[q];
+    maxR = std::max(maxR, res.R[q]);
+  }
+  res.big = DeviceBuffer<uint64_t>(std::max<uint64_t>(total, 1), st);
+  DeviceBuffer<uint64_t> dbase(nq, st);
+  DeviceBuffer<uint32_t> dcap(nq, st), dlist(nre, st);
+  MIHG_CUDA(cudaMemcpyAsync(dbase.get(), res.base.data(), nq * 8, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemcpyAsync(dcap.get(), hcap.data(), nq * 4, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemcpyAsync(dlist.get(), res.list.data(), nre * 4, cudaMemcpyHostToDevice, st));
+  MIHG_CUDA(cudaMemsetAsync(ws.bufcnt.get(), 0, nq * 4, st));
+  ProbeArgs rp = p;
+  rp.hist = nullptr;
+  rp.trc = nullptr;
+  rp.ubound = ws.final_r.get();
+  rp.rlimit = ws.final_r.get();
+  rp.buf = res.big.get();
+  rp.bufbase = dbase.get();
+  rp.bufcap = dcap.get();
+  rp.active = dlist.get();
+  for (uint32_t r = 0; r <= maxR; ++r) {
+    const uint32_t a = r % m, rr = r / m, s = idx.lengths[a];
+    const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
+    if (!ring) continue;
+    rp.tab = idx.tables[a]->view();
+    rp.a = a;
+    rp.rr = rr;
+    rp.r = r;
+    rp.ring = ring;
+    plan_round(rp, nre);
+    plan_slicing(rp, ws, nre, st);
+    dispatch_probe(rp, false, st);
+  }
+  MIHG_CUDA(cudaStreamSynchronize(st));
+  return res;
+}
+
 void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_t* d_ids,
                uint32_t* d_dists, Trace* d_tr, cudaStream_t st, const KnnOptions& opt) {
   Workspace& ws = *idx.ws;
@@ -766,26 +855,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
                                        ws.dropmin.get(), ws.act0.get(), ws.final_r.get());
   MIHG_LAUNCH();
 
-  ProbeArgs p{};
-  p.codes = idx.codes.get();
-  p.qcodes = d_q;
-  p.qsub = ws.qsub.get();
-  p.subs = idx.d_subs.get();
-  p.submask = idx.d_submask.get();
-  p.m = m;
-  p.nw = idx.W;
-  p.hist = ws.hist.get();
-  p.b1 = b1;
-  p.ubound = ws.ubound.get();
-  p.buf = ws.buf.get();
-  p.cap_fixed = cap;
-  p.bufcnt = ws.bufcnt.get();
-  p.dropmin = ws.dropmin.get();
-  p.trc = ws.trc.get();
-  p.pieces = ws.pieces.get();
-  p.piece_count = ws.piece_count.get();
-  p.piece_cap = kPieceQueue;
-  p.binom = device_binomials();
+  ProbeArgs p = make_probe_args(idx, ws, d_q);
 
   std::vector<uint64_t> lookups_prefix;
   uint32_t* act_in = ws.act0.get();
@@ -852,51 +922,12 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   select_topk(sa, uint32_t(nq), st);
 
   if (nre == 0) return;
-  // Re-run: exact-size buffers, bound = final radius, no histogram / trace updates.
-  std::vector<uint32_t> hre(nre), hneed(nq), hR(nq);
-  MIHG_CUDA(cudaMemcpyAsync(hre.data(), rerun.get(), nre * 4, cudaMemcpyDeviceToHost, st));
-  MIHG_CUDA(cudaMemcpyAsync(hneed.data(), need.get(), nq * 4, cudaMemcpyDeviceToHost, st));
-  MIHG_CUDA(cudaMemcpyAsync(hR.data(), ws.final_r.get(), nq * 4, cudaMemcpyDeviceToHost, st));
-  MIHG_CUDA(cudaStreamSynchronize(st));
-  std::sort(hre.begin(), hre.end());
-  std::vector<uint64_t> hbase(nq, 0);
-  std::vector<uint32_t> hcap(nq, 0);
-  uint64_t total = 0;
-  uint32_t maxR = 0;
-  for (uint32_t q : hre) {
-    hbase[q] = total;
-    hcap[q] = hneed[q];
-    total += hneed[q];
-    maxR = std::max(maxR, hR[q]);
-  }
-  DeviceBuffer<uint64_t> big(std::max<uint64_t>(total, 1), st), dbase(nq, st);
-  DeviceBuffer<uint32_t> dcap(nq, st), dlist(nre, st);
-  MIHG_CUDA(cudaMemcpyAsync(dbase.get(), hbase.data(), nq * 8, cudaMemcpyHostToDevice, st));
-  MIHG_CUDA(cudaMemcpyAsync(dcap.get(), hcap.data(), nq * 4, cudaMemcpyHostToDevice, st));
-  MIHG_CUDA(cudaMemcpyAsync(dlist.get(), hre.data(), nre * 4, cudaMemcpyHostToDevice, st));
-  MIHG_CUDA(cudaMemsetAsync(ws.bufcnt.get(), 0, nq * 4, st));
-  ProbeArgs rp = p;
-  rp.hist = nullptr;
-  rp.trc = nullptr;
-  rp.ubound = ws.final_r.get();
-  rp.rlimit = ws.final_r.get();
-  rp.buf = big.get();
-  rp.bufbase = dbase.get();
-  rp.bufcap = dcap.get();
-  rp.active = dlist.get();
-  for (uint32_t r = 0; r <= maxR; ++r) {
-    const uint32_t a = r % m, rr = r / m, s = idx.lengths[a];
-    const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
-    if (!ring) continue;
-    rp.tab = idx.tables[a]->view();
-    rp.a = a;
-    rp.rr = rr;
-    rp.r = r;
-    rp.ring = ring;
-    plan_round(rp, nre);
-    plan_slicing(rp, ws, nre, st);
-    dispatch_probe(rp, false, st);
-  }
+  RerunResult rr_res = rerun_pass(idx, p, rerun.get(), nre, need.get(), nq, st);
+  std::vector<uint32_t>& hre = rr_res.list;
+  std::vector<uint64_t>& hbase = rr_res.base;
+  std::vector<uint32_t>& hneed = rr_res.need;
+  std::vector<uint32_t>& hR = rr_res.R;
+  DeviceBuffer<uint64_t>& big = rr_res.big;
   // select the re-run queries from their exact buffers
   DeviceBuffer<uint64_t> rows(nre, st), sbase(nre, st);
   DeviceBuffer<uint32_t> scount(nre, st), smaxd(nre, st);
@@ -942,6 +973,179 @@ void knn_device(Index& idx, const uint64_t* d_queries, uint64_t nq, uint32_t k, 
     const uint64_t cn = std::min(chunk, nq - q0);
     knn_chunk(idx, d_queries + q0 * idx.W, cn, k, d_ids + q0 * k, d_dists + q0 * k,
               d_traces ? d_traces + q0 : nullptr, st, opt);
+  }
+}
+
+
+// ---- range_search (index.hpp:149-176, paper Alg. 2) --------------------------------------------
+// Steps 0..r of the kNN loop probe exactly the reference's split balls (table j gets rings
+// 0..floor((r-j)/m), i.e. ball(r') for j <= a and ball(r'-1) for j > a with r = m r' + a), so
+// range search is those rounds with the bound fixed at U = r and no stopping test; every key with
+// d <= r is kept and the result is sorted by (dist, id) with one radix sort of
+// (query << 45 | dist << 32 | id) keys.
+namespace {
+
+__global__ void range_init_kernel(uint64_t nq, uint32_t r, uint32_t* ubound, uint32_t* bufcnt,
+                                  uint32_t* dropmin, uint32_t* act, uint32_t* final_r) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < nq;
+       q += uint64_t(gridDim.x) * blockDim.x) {
+    ubound[q] = r;
+    bufcnt[q] = 0;
+    dropmin[q] = 0xFFFFFFFFu;
+    act[q] = uint32_t(q);
+    final_r[q] = r;
+  }
+}
+
+__global__ void range_compose_kernel(const uint64_t* __restrict__ buf, uint32_t cap,
+                                     const uint32_t* __restrict__ seg_count,
+                                     const uint64_t* __restrict__ rbase, const uint64_t* __restrict__ big,
+                                     const uint32_t* __restrict__ need,
+                                     const uint64_t* __restrict__ out_off, uint32_t r,
+                                     uint64_t* __restrict__ out_keys) {
+  __shared__ uint32_t s_at;
+  const uint64_t q = blockIdx.x;
+  const bool rerun = rbase && rbase[q] != ~0ull;
+  const uint64_t* src = rerun ? big + rbase[q] : buf + q * cap;
+  const uint32_t cnt = rerun ? need[q] : seg_count[q];
+  if (threadIdx.x == 0) s_at = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint64_t key = src[i];
+    if (uint32_t(key >> 32) <= r) out_keys[out_off[q] + atomicAdd(&s_at, 1u)] = (q << 45) | key;
+  }
+}
+
+__global__ void range_split_kernel(const uint64_t* __restrict__ keys, uint64_t total, uint32_t id_base,
+                                   uint32_t* __restrict__ ids, uint32_t* __restrict__ dists) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    ids[i] = uint32_t(keys[i]) + id_base;
+    dists[i] = uint32_t(keys[i] >> 32) & 0x1FFFu;
+  }
+}
+
+__global__ void range_trace_fix_kernel(uint64_t nq, Trace* traces) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < nq;
+       q += uint64_t(gridDim.x) * blockDim.x)
+    traces[q].final_radius = 0;  // SearchTrace::final_radius is kNN-only (index.hpp:50)
+}
+
+}  // namespace
+
+// One chunk of queries; returns per-query result counts (host) and the sorted device results.
+void range_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t r, std::vector<uint64_t>& counts,
+                 DeviceBuffer<uint32_t>& out_ids, DeviceBuffer<uint32_t>& out_dists, Trace* d_tr,
+                 cudaStream_t st) {
+  Workspace& ws = *idx.ws;
+  const uint32_t m = idx.m, b1 = idx.bits + 1, cap = ws.cap;
+  const unsigned g1 = unsigned(std::min<uint64_t>((nq + 255) / 256, 4096));
+  extract_all_keys(idx, d_q, nq, ws.qsub.get(), st);
+  MIHG_CUDA(cudaMemsetAsync(ws.hist.get(), 0, nq * b1 * 4, st));
+  MIHG_CUDA(cudaMemsetAsync(ws.trc.get(), 0, 2 * nq * 8, st));
+  range_init_kernel<<<g1, 256, 0, st>>>(nq, r, ws.ubound.get(), ws.bufcnt.get(), ws.dropmin.get(),
+                                         ws.act0.get(), ws.final_r.get());
+  MIHG_LAUNCH();
+  ProbeArgs p = make_probe_args(idx, ws, d_q);
+  std::vector<uint64_t> lookups_prefix;
+  uint64_t acc = 0;
+  for (uint32_t t = 0; t <= r; ++t) {
+    const uint32_t a = t % m, rr = t / m, s = idx.lengths[a];
+    const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
+    acc += ring;
+    lookups_prefix.push_back(acc);
+    if (!ring) continue;
+    p.tab = idx.tables[a]->view();
+    p.a = a;
+    p.rr = rr;
+    p.r = t;
+    p.active = ws.act0.get();
+    p.ring = ring;
+    plan_round(p, nq);
+    plan_slicing(p, ws, nq, st);
+    dispatch_probe(p, d_tr != nullptr, st);
+  }
+  MIHG_CUDA(cudaMemcpyAsync(ws.lookups_prefix.get(), lookups_prefix.data(), lookups_prefix.size() * 8,
+                            cudaMemcpyHostToDevice, st));
+  DeviceBuffer<uint32_t> seg_count(nq, st), need(nq, st), rerun(nq, st);
+  MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
+  mih_finish_kernel<<<g1, 256, 0, st>>>(nq, ws.final_r.get(), ws.hist.get(), b1, ws.bufcnt.get(), cap,
+                                        ws.dropmin.get(), ws.trc.get(), ws.lookups_prefix.get(), d_tr,
+                                        seg_count.get(), need.get(), rerun.get(), ws.counters.get());
+  MIHG_LAUNCH();
+  if (d_tr) {
+    range_trace_fix_kernel<<<g1, 256, 0, st>>>(nq, d_tr);
+    MIHG_LAUNCH();
+  }
+  const uint32_t nre = read_counter(ws.counters.get(), ws.h_counter, st);
+  std::vector<uint32_t> hneed(nq);
+  MIHG_CUDA(cudaMemcpyAsync(hneed.data(), need.get(), nq * 4, cudaMemcpyDeviceToHost, st));
+  MIHG_CUDA(cudaStreamSynchronize(st));
+  RerunResult rr_res;
+  DeviceBuffer<uint64_t> rbase;
+  if (nre) {
+    rr_res = rerun_pass(idx, p, rerun.get(), nre, need.get(), nq, st);
+    std::vector<uint64_t> hb(nq, ~0ull);
+    for (uint32_t q : rr_res.list) hb[q] = rr_res.base[q];
+    rbase = DeviceBuffer<uint64_t>(nq, st);
+    MIHG_CUDA(cudaMemcpyAsync(rbase.get(), hb.data(), nq * 8, cudaMemcpyHostToDevice, st));
+  }
+  counts.assign(nq, 0);
+  std::vector<uint64_t> off(nq);
+  uint64_t total = 0;
+  for (uint64_t q = 0; q < nq; ++q) {
+    off[q] = total;
+    counts[q] = hneed[q];
+    total += hneed[q];
+  }
+  DeviceBuffer<uint64_t> d_off(nq, st), keys(std::max<uint64_t>(total, 1), st);
+  MIHG_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), nq * 8, cudaMemcpyHostToDevice, st));
+  range_compose_kernel<<<unsigned(nq), 256, 0, st>>>(ws.buf.get(), cap, seg_count.get(), rbase.get(),
+                                                      rr_res.big.get(), need.get(), d_off.get(), r,
+                                                      keys.get());
+  MIHG_LAUNCH();
+  uint32_t qbits = 0;
+  while ((uint64_t(1) << qbits) < nq) ++qbits;
+  radix_sort_keys_u64(keys.get(), total, 45 + qbits, st);
+  out_ids = DeviceBuffer<uint32_t>(std::max<uint64_t>(total, 1), st);
+  out_dists = DeviceBuffer<uint32_t>(std::max<uint64_t>(total, 1), st);
+  if (total) {
+    range_split_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 65535)), 256, 0, st>>>(
+        keys.get(), total, idx.id_base, out_ids.get(), out_dists.get());
+    MIHG_LAUNCH();
+  }
+  MIHG_CUDA(cudaStreamSynchronize(st));
+}
+
+void range_host(Index& idx, const uint64_t* h_q, uint64_t nq, uint32_t r, uint64_t* h_offsets,
+                uint32_t* h_ids, uint32_t* h_dists, uint64_t capacity, Trace* h_tr, cudaStream_t st,
+                const KnnOptions& opt) {
+  if (r > idx.bits) throw InvalidArgument("range_search: radius exceeds code width");
+  h_offsets[0] = 0;
+  if (nq == 0) return;
+  const uint64_t chunk = std::min<uint64_t>(nq, std::min<uint64_t>(opt.query_chunk, uint64_t(1) << 18));
+  ensure_workspace(idx, chunk, opt.buffer_cap, st);
+  DeviceBuffer<uint64_t> dq(chunk * idx.W, st);
+  DeviceBuffer<Trace> dt(h_tr ? chunk : 0, st);
+  uint64_t written = 0;
+  for (uint64_t q0 = 0; q0 < nq; q0 += chunk) {
+    const uint64_t cn = std::min(chunk, nq - q0);
+    MIHG_CUDA(cudaMemcpyAsync(dq.get(), h_q + q0 * idx.W, cn * idx.W * 8, cudaMemcpyHostToDevice, st));
+    std::vector<uint64_t> counts;
+    DeviceBuffer<uint32_t> ids, dists;
+    range_chunk(idx, dq.get(), cn, r, counts, ids, dists, h_tr ? dt.get() : nullptr, st);
+    uint64_t tot = 0;
+    for (uint64_t q = 0; q < cn; ++q) {
+      tot += counts[q];
+      h_offsets[q0 + q + 1] = written + tot;
+    }
+    if (h_ids && written + tot <= capacity && tot) {
+      MIHG_CUDA(cudaMemcpyAsync(h_ids + written, ids.get(), tot * 4, cudaMemcpyDeviceToHost, st));
+      MIHG_CUDA(cudaMemcpyAsync(h_dists + written, dists.get(), tot * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (h_tr) MIHG_CUDA(cudaMemcpyAsync(h_tr + q0, dt.get(), cn * sizeof(Trace), cudaMemcpyDeviceToHost, st));
+    MIHG_CUDA(cudaStreamSynchronize(st));
+    written += tot;
   }
 }
 

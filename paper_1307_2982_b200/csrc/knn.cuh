@@ -20,6 +20,12 @@ struct KnnOptions {
 void knn_device(Index& idx, const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
                 uint32_t* d_dists, Trace* d_traces, cudaStream_t st, const KnnOptions& opt = {});
 
+// Batched MihIndex::range_search (index.hpp:149-176) with host buffers: offsets[nq+1] always
+// written; ids/dists (capacity entries) written when offsets[nq] <= capacity.
+void range_host(Index& idx, const uint64_t* h_queries, uint64_t nq, uint32_t r, uint64_t* h_offsets,
+                uint32_t* h_ids, uint32_t* h_dists, uint64_t capacity, Trace* h_traces, cudaStream_t st,
+                const KnnOptions& opt = {});
+
 // Batched scan_knn (scan.hpp:43-68) over the index's device-resident codes.
 void scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
                      const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,

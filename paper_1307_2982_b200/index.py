@@ -246,6 +246,39 @@ class MihIndex:
                                                     C.c_void_p(d_traces) if d_traces else None,
                                                     C.c_void_p(stream) if stream else None))
 
+    def range_search(self, q: BinaryCode, r: int, trace: SearchTrace | None = None, scratch=None):
+        """index.hpp:149-176: exactly {(i, d_i) : d_i <= r}, sorted by (distance, id)."""
+        if q.bits != self._bits:
+            raise ValueError("range_search: query width mismatch")
+        offs, ids, dists, tr = self.range_search_batch(q.words.reshape(1, -1), r, with_trace=trace is not None)
+        if trace is not None:
+            t = tr[0]
+            trace.lookups, trace.candidates = int(t.lookups), int(t.candidates)
+            trace.unique_candidates = int(t.unique_candidates)
+            trace.distance_evaluations = int(t.distance_evaluations)
+            trace.final_radius = int(t.final_radius)
+        return [Neighbor(int(i), int(d)) for i, d in zip(ids, dists)]
+
+    def range_search_batch(self, queries, r: int, with_trace: bool = False):
+        """Returns (offsets[nq+1], ids, dists, traces|None): query i's neighbours are
+        ids[offsets[i]:offsets[i+1]] in (dist, id) order."""
+        q = self._queries(queries)
+        nq = q.shape[0]
+        if r > self._bits:
+            raise ValueError("range_search: radius exceeds code width")
+        offs = np.zeros(nq + 1, np.uint64)
+        tr = (_lib.Trace * max(nq, 1))() if with_trace else None
+        L = _lib.lib()
+        cap = min(self._n * nq, 1 << 22)
+        while True:
+            ids = np.zeros(max(cap, 1), np.uint32)
+            dists = np.zeros(max(cap, 1), np.uint32)
+            _lib.check(L.mihg_range_batch(self._h, _p64(q), nq, r, _p64(offs), _p32(ids), _p32(dists), cap, tr))
+            total = int(offs[nq])
+            if total <= cap:
+                return offs, ids[:total], dists[:total], tr
+            cap = total
+
     def scan_knn_batch(self, queries, k: int):
         """Exhaustive GPU comparator over the index's codes (scan.hpp:43-68 semantics)."""
         q = self._queries(queries)

@@ -246,3 +246,40 @@ def test_table_stats_match_reference(cuda_ok, golden, layout):
             st = idx.table(j).stats()
             got = [st.non_empty_buckets, st.max_bucket_size, st.total_entries, st.estimated_bytes]
             assert got == [int(x) for x in d[name][j]], (name, j)
+
+
+@pytest.mark.parametrize("layout", ["auto", "sparse"])
+@pytest.mark.parametrize("bits", [32, 96, 100])
+def test_range_search_matches_reference(cuda_ok, golden, bits, layout):
+    # index_test.cpp:96-112 RangeMatchesScanRandomized + acceptance criteria 1/4 (probe counts):
+    # ids, dists and lookups/candidates/unique identical to MihIndex::range_search
+    mg = _mg()
+    d = golden(f"range_b{bits}")
+    for m in (2, 4, 5):
+        if (bits + m - 1) // m > 32 or (layout == "sparse" and bits // m < 6):
+            continue
+        idx = mg.MihIndex.build(mg.CodeDatabase(bits, d["codes"]), mg.consecutive_partition(bits, m),
+                                layout=layout)
+        for r in (0, 1, 5, bits // 3):
+            offs, ids, dists, tr = idx.range_search_batch(d["queries"], r, with_trace=True)
+            assert np.array_equal(offs, d[f"m{m}_r{r}_offs"]), (m, r)
+            assert np.array_equal(ids, d[f"m{m}_r{r}_ids"]), (m, r)
+            assert np.array_equal(dists, d[f"m{m}_r{r}_dists"]), (m, r)
+            assert np.array_equal(_trace_array(tr)[:, :4], d[f"m{m}_r{r}_trace"][:, :4]), (m, r)
+            assert not _trace_array(tr)[:, 4].any()
+
+
+def test_final_radius_is_a_completeness_certificate(cuda_ok):
+    # index_test.cpp:186-206: the k results are the head of range_search(final_radius)
+    mg = _mg()
+    db = mg.gen_uniform(2000, 64, 12)
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(64, 4))
+    qs = mg.gen_uniform(10, 64, 13)
+    for qi in range(10):
+        tr = mg.SearchTrace()
+        res = idx.knn_search(qs.code(qi), 10, tr)
+        assert res[-1].dist <= tr.final_radius
+        within = idx.range_search(qs.code(qi), tr.final_radius)
+        assert len(within) >= 10 and within[:10] == res
+    with pytest.raises(ValueError):
+        idx.range_search(qs.code(0), 65)  # radius exceeds code width (index.hpp:152)

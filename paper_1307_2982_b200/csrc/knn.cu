@@ -47,7 +47,8 @@ struct Workspace {
   DeviceBuffer<uint64_t> lookups_prefix;
   DeviceBuffer<Piece> pieces;
   DeviceBuffer<uint32_t> piece_count;
-  DeviceBuffer<uint64_t> slice_cnt, slice_prefix, work_total;
+  DeviceBuffer<uint32_t> gstart, grouped;
+  DeviceBuffer<uint64_t> pair_prefix;
   DeviceBuffer<unsigned long long> work_counter;
   uint32_t* h_counter = nullptr;
   cudaStream_t st = nullptr;
@@ -203,37 +204,84 @@ struct ProbeArgs {
   uint32_t* piece_count;
   uint32_t piece_cap;
   const uint64_t* binom;    // device_binomials()
-  // L2-sliced rounds (slice_bits > 0): units enumerated per (slice P, active slot), P-major
+  // L2-sliced rounds (slice_bits > 0): active queries grouped by the top t bits G of their
+  // substring; units enumerated per (slice P, group G) pair, P-major, claimed in order.
   uint32_t slice_bits;
-  uint64_t nact, npairs;
-  const uint64_t* unit_prefix;  // exclusive prefix of units per pair (npairs)
-  const uint64_t* work_total;   // total units (device)
+  const uint64_t* pair_prefix;  // 4^t + 1 exclusive unit prefix over (P, G) pairs
+  const uint32_t* gstart;       // 2^t + 1 group starts into grouped[]
+  const uint32_t* grouped;      // active slots sorted by group
   unsigned long long* work_counter;
 };
 
-// Units per (slice P, active slot) of a sliced round: the ring's sub-ring inside slice P has
-// the top flip pattern T = P ^ (q_a >> s') fixed and rr - popc(T) flips in the low s' bits.
-__global__ void slice_units_kernel(ProbeArgs p, uint64_t span, uint64_t* __restrict__ cnt) {
-  const uint32_t sb = p.tab.s - p.slice_bits;
-  for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < p.npairs;
-       idx += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t P = uint32_t(idx / p.nact);
-    const uint64_t slot = idx - uint64_t(P) * p.nact;
-    const uint32_t q = p.active[slot];
-    uint64_t c = 0;
-    if (!(p.rlimit && p.r > p.rlimit[q])) {
-      const uint32_t h = __popc(P ^ (p.qsub[uint64_t(q) * p.m + p.a] >> sb));
-      if (h <= p.rr && p.rr - h <= sb) c = (p.binom[sb * kBinomStride + (p.rr - h)] + span - 1) / span;
+// Per sliced round (one block): group the active queries by G = top t bits of their substring,
+// then the unit prefix over (P, G) pairs: within slice P a query of group G has the sub-ring
+// with top flip pattern T = P ^ G fixed and rr - popc(T) flips in the low s' = s - t bits.
+__global__ void __launch_bounds__(1024) slice_plan_kernel(ProbeArgs p, uint32_t nact, uint64_t span,
+                                                          uint32_t* __restrict__ gstart,
+                                                          uint32_t* __restrict__ grouped,
+                                                          uint64_t* __restrict__ pair_prefix) {
+  __shared__ uint32_t hist[256], cur[256];
+  __shared__ unsigned long long part[1024];
+  const uint32_t t = p.slice_bits, G = 1u << t, sb = p.tab.s - t;
+  for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nact; i += blockDim.x) {
+    const uint32_t q = p.active[i];
+    if (p.rlimit && p.r > p.rlimit[q]) continue;
+    atomicAdd(&hist[p.qsub[uint64_t(q) * p.m + p.a] >> sb], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (uint32_t g = 0; g < G; ++g) {
+      gstart[g] = acc;
+      cur[g] = acc;
+      acc += hist[g];
     }
-    cnt[idx] = c;
+    gstart[G] = acc;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nact; i += blockDim.x) {
+    const uint32_t q = p.active[i];
+    if (p.rlimit && p.r > p.rlimit[q]) continue;
+    grouped[atomicAdd(&cur[p.qsub[uint64_t(q) * p.m + p.a] >> sb], 1u)] = i;
+  }
+  // units per pair, then a block-wide exclusive scan in P-major order
+  const uint32_t npairs = G * G, per = (npairs + blockDim.x - 1) / blockDim.x;
+  unsigned long long run = 0;
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t idx = threadIdx.x * per + j;
+    if (idx >= npairs) break;
+    const uint32_t P = idx >> t, g = idx & (G - 1), h = __popc(P ^ g);
+    uint64_t c = 0;
+    if (h <= p.rr && p.rr - h <= sb)
+      c = uint64_t(hist[g]) * ((p.binom[sb * kBinomStride + (p.rr - h)] + span - 1) / span);
+    pair_prefix[idx] = c;  // temporarily the count
+    run += c;
+  }
+  part[threadIdx.x] = run;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long acc = 0;
+    for (uint32_t i = 0; i < blockDim.x; ++i) {
+      const unsigned long long v = part[i];
+      part[i] = acc;
+      acc += v;
+    }
+    pair_prefix[npairs] = acc;
+    *p.work_counter = 0;
+  }
+  __syncthreads();
+  unsigned long long acc = part[threadIdx.x];
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t idx = threadIdx.x * per + j;
+    if (idx >= npairs) break;
+    const uint64_t c = pair_prefix[idx];
+    pair_prefix[idx] = acc;
+    acc += c;
   }
 }
 
-__global__ void slice_total_kernel(const uint64_t* __restrict__ prefix, const uint64_t* __restrict__ cnt,
-                                   uint64_t npairs, uint64_t* total, unsigned long long* counter) {
-  *total = prefix[npairs - 1] + cnt[npairs - 1];
-  *counter = 0;
-}
 
 // Is step (a, rr) the first step that reaches a candidate whose substring distances are d_j?
 // New iff for j < a: d_j > rr, and for j > a: d_j >= rr (r == min_j m*d_j + j).
@@ -351,21 +399,24 @@ __global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kerne
       // one L2-sized slice of the table at a time
       if (lane == 0) u = atomicAdd(p.work_counter, 1ull);
       u = __shfl_sync(~0u, u, 0);
-      if (u >= *p.work_total) break;
-      uint64_t lo_i = 0, hi_i = p.npairs;  // last pair with prefix <= u
+      const uint32_t npairs = 1u << (2 * p.slice_bits);
+      if (u >= __ldg(p.pair_prefix + npairs)) break;
+      uint32_t lo_i = 0, hi_i = npairs;  // last pair with prefix <= u (L1-resident table)
       while (hi_i - lo_i > 1) {
-        const uint64_t mid = (lo_i + hi_i) >> 1;
-        if (__ldg(p.unit_prefix + mid) <= u) lo_i = mid;
+        const uint32_t mid = (lo_i + hi_i) >> 1;
+        if (__ldg(p.pair_prefix + mid) <= u) lo_i = mid;
         else hi_i = mid;
       }
-      const uint32_t P = uint32_t(lo_i / p.nact);
-      slot = lo_i - uint64_t(P) * p.nact;
-      part = u - __ldg(p.unit_prefix + lo_i);
+      const uint32_t P = lo_i >> p.slice_bits, G = lo_i & ((1u << p.slice_bits) - 1);
       sbits = p.tab.s - p.slice_bits;
-      const uint32_t qa0 = p.qsub[uint64_t(p.active[slot]) * p.m + p.a];
-      const uint32_t T = P ^ (qa0 >> sbits);  // flip pattern of the top slice bits
-      zbits = p.rr - __popc(T);               // count kernel guarantees 0 <= zbits <= sbits
+      const uint32_t T = P ^ G;  // flip pattern of the top slice bits
+      zbits = p.rr - __popc(T);
       ring = __ldg(p.binom + sbits * kBinomStride + zbits);
+      const uint64_t upq = (ring + span - 1) / span;
+      const uint64_t rel = u - __ldg(p.pair_prefix + lo_i);
+      const uint64_t kq = rel / upq;
+      part = rel - kq * upq;
+      slot = p.grouped[p.gstart[G] + kq];
       high = uint64_t(T) << sbits;
     } else {
       if (u >= p.total) break;
@@ -666,16 +717,34 @@ void plan_round(ProbeArgs& p, uint64_t nact) {
   p.total = nact * p.cpq;
 }
 
-// L2-sliced probing for tables whose probe structure exceeds L2 (north_star: the 32-bit sparse
-// tables): pick t so one slice of the directory/offsets is <= 32 MB, for rounds large enough
-// (>= 4M probes) to amortise the per-(slice, query) unit table. Experimental, off by default
-// (MIHG_SLICE=1 enables): measured slower on config 4 (unit decode cost).
+// Key-sliced probing for tables whose probe structure is much larger than L2/TLB reach (the
+// 32-bit sparse tables of configs 4/5): the ring of every query splits exactly by the top t key
+// bits, so a round's work is ordered slice-major and the warps in flight probe one ~128 MB
+// region of the directory (and of the table-order codes) at a time. Measured on config 4:
+// 546K -> 706K q/s (slice 128 MB, ~128 MB in flight; sweep in DESIGN.md §3). MIHG_SLICE=0
+// disables; MIHG_SLICE_MB / MIHG_INFLIGHT_MB tune.
 bool slicing_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("MIHG_SLICE");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
+}
+
+double slice_mb() {
+  static const double v = [] {
+    const char* e = std::getenv("MIHG_SLICE_MB");
+    return e ? std::atof(e) : 128.0;
+  }();
+  return v;
+}
+
+double inflight_mb() {
+  static const double v = [] {
+    const char* e = std::getenv("MIHG_INFLIGHT_MB");
+    return e ? std::atof(e) : 128.0;
+  }();
+  return v;
 }
 
 void plan_slicing(ProbeArgs& p, Workspace& ws, uint64_t nact, cudaStream_t st) {
@@ -685,32 +754,24 @@ void plan_slicing(ProbeArgs& p, Workspace& ws, uint64_t nact, cudaStream_t st) {
                                    : double(uint64_t(1) << (s - kDirBucketsLog2)) * sizeof(DirBlock);
   if (!slicing_enabled() || bytes <= 64.0 * (1 << 20) || double(nact) * double(p.ring) < 4.0e6) return;
   uint32_t t = 0;
-  while (bytes / double(1u << t) > 32.0 * (1 << 20) && t < 12) ++t;
+  while (bytes / double(1u << t) > slice_mb() * (1 << 20) && t < 8) ++t;
   t = std::min<uint32_t>(t, s - 1);
-  while (t > 0 && (uint64_t(nact) << t) > (uint64_t(1) << 23)) --t;  // bound the unit table
   if (t == 0) return;
-  const uint64_t npairs = uint64_t(nact) << t;
-  if (ws.slice_cnt.size() < npairs) {
-    ws.slice_cnt = DeviceBuffer<uint64_t>(npairs, st);
-    ws.slice_prefix = DeviceBuffer<uint64_t>(npairs, st);
-  }
-  // Keep the in-flight wavefront inside one slice: units per slice >= 4x the resident warps.
+  // the in-flight wavefront may span `inflight` slices (~half of L2): units per slice >=
+  // resident warps / inflight
   const double resident_warps = double(device_sm_count()) * 64;
+  const double inflight = std::max(1.0, std::floor(inflight_mb() * (1 << 20) / (bytes / double(1u << t))));
   const double lanes_per_slice = double(nact) * double(p.ring) / double(1u << t);
-  const double chunk = std::floor(lanes_per_slice / (4.0 * resident_warps * 32.0));
+  const double chunk = std::floor(lanes_per_slice * inflight / (resident_warps * 32.0));
   p.chunk = uint32_t(std::max(1.0, std::min(chunk, 256.0)));
   p.slice_bits = t;
-  p.nact = nact;
-  p.npairs = npairs;
-  p.unit_prefix = ws.slice_prefix.get();
-  p.work_total = ws.work_total.get();
+  if (ws.grouped.size() < nact) ws.grouped = DeviceBuffer<uint32_t>(nact, st);
+  p.gstart = ws.gstart.get();
+  p.grouped = ws.grouped.get();
+  p.pair_prefix = ws.pair_prefix.get();
   p.work_counter = ws.work_counter.get();
-  const uint64_t span = uint64_t(p.chunk) * 32;
-  slice_units_kernel<<<unsigned(std::min<uint64_t>((npairs + 255) / 256, 8192)), 256, 0, st>>>(p, span, ws.slice_cnt.get());
-  MIHG_LAUNCH();
-  exclusive_scan<uint64_t>(ws.slice_cnt.get(), ws.slice_prefix.get(), npairs, st);
-  slice_total_kernel<<<1, 1, 0, st>>>(ws.slice_prefix.get(), ws.slice_cnt.get(), npairs, ws.work_total.get(),
-                                      ws.work_counter.get());
+  slice_plan_kernel<<<1, 1024, 0, st>>>(p, uint32_t(nact), uint64_t(p.chunk) * 32, ws.gstart.get(),
+                                        ws.grouped.get(), ws.pair_prefix.get());
   MIHG_LAUNCH();
 }
 
@@ -741,7 +802,8 @@ void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
   ws->lookups_prefix = DeviceBuffer<uint64_t>(b1 + 1, st);
   ws->pieces = DeviceBuffer<Piece>(kPieceQueue, st);
   ws->piece_count = DeviceBuffer<uint32_t>(1, st);
-  ws->work_total = DeviceBuffer<uint64_t>(1, st);
+  ws->gstart = DeviceBuffer<uint32_t>(257, st);
+  ws->pair_prefix = DeviceBuffer<uint64_t>((1u << 16) + 1, st);
   ws->work_counter = DeviceBuffer<unsigned long long>(1, st);
   MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_counter), 16));
   MIHG_CUDA(cudaEventCreate(&ws->ev0));

@@ -38,7 +38,7 @@ struct ScanArgs {
 };
 
 // In-place exact top-k of a warp's list (ids ascending in list order); returns the new bound.
-__device__ uint32_t compact_list(uint64_t* list, uint32_t& cnt, uint32_t tau, uint32_t k,
+__device__ __noinline__ uint32_t compact_list(uint64_t* list, uint32_t& cnt, uint32_t tau, uint32_t k,
                                  uint32_t* hist) {
   const uint32_t lane = threadIdx.x & 31;
   MIHG_DASSERT(tau < 4097);
@@ -115,29 +115,45 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(ScanArgs a) {
     return a.lists + ((q0 + t) * a.slots + slot) * uint64_t(a.L);
   };
   const uint32_t lt = lanemask_lt();
+  // register double buffer: the next 32 codes are in flight while this chunk is tested
+  uint64_t xn[W ? W : 1];
+  if constexpr (W > 0) {
+    if (lo < hi) load_code<W>(a.codes, min(lo + lane, hi - 1), xn);
+  }
   for (uint64_t base = lo; base < hi; base += 32) {
     const uint64_t id = base + lane;
     const bool valid = id < hi;
     uint64_t x[W ? W : 1];
     const uint64_t* xp = a.codes + (valid ? id : lo) * nw;
-    if constexpr (W > 0) load_code<W>(a.codes, valid ? id : lo, x);
+    if constexpr (W > 0) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) x[w] = xn[w];
+      if (base + 32 < hi) load_code<W>(a.codes, min(base + 32 + lane, hi - 1), xn);
+    }
+    uint32_t d[QT];
+    bool anyp = false;
 #pragma unroll
     for (int t = 0; t < QT; ++t) {
-      uint32_t d;
       if constexpr (W > 0) {
-        d = hamming<W>(qr[t], x, W);
+        d[t] = hamming<W>(qr[t], x, W);
       } else {
         const uint64_t* qp = a.queries + min(q0 + t, a.nq - 1) * nw;
-        d = 0;
-        for (uint32_t w = 0; w < nw; ++w) d += __popcll(__ldg(qp + w) ^ __ldg(xp + w));
+        uint32_t dd = 0;
+        for (uint32_t w = 0; w < nw; ++w) dd += __popcll(__ldg(qp + w) ^ __ldg(xp + w));
+        d[t] = dd;
       }
-      const bool pass = valid && d <= tau[t] && tau[t] != 0xFFFFFFFFu;
+      anyp |= valid && d[t] <= tau[t];  // padding queries have tau = 0xFFFFFFFF: checked below
+    }
+    if (!__any_sync(~0u, anyp)) continue;  // fast path: nothing in this chunk beats any bound
+#pragma unroll
+    for (int t = 0; t < QT; ++t) {
+      const bool pass = valid && d[t] <= tau[t] && tau[t] != 0xFFFFFFFFu;
       const uint32_t bal = __ballot_sync(~0u, pass);
       if (bal) {
         uint64_t* list = list_of(t);
         MIHG_DASSERT(q0 + t < a.nq);
         MIHG_DASSERT(cnt[t] + 32 <= a.L);
-        if (pass) list[cnt[t] + __popc(bal & lt)] = (uint64_t(d) << 32) | uint32_t(id);
+        if (pass) list[cnt[t] + __popc(bal & lt)] = (uint64_t(d[t]) << 32) | uint32_t(id);
         cnt[t] += __popc(bal);
         if (cnt[t] >= 2 * a.k) {
           __syncwarp();

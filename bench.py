@@ -410,20 +410,25 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else 0.0
-    if args.method == "scan":
+    switched = (prof1.switched_queries - prof0.switched_queries) / args.steps
+    if args.method == "scan" or switched >= 0.5 * nq:
         # K6 is POPC-bound: n*W popc64 = 2*n*W POPC32 per query; peak = 16 POPC/clk/SM measured
         # 4.56e12/s at 1.925 GHz (tools/probe/ubench.cu), scaled to the sampled SM clock.
         pc_peak = 4.56e12 * ((clk.get("sm_mhz") or 1925.0) / 1925.0)
         pc_ach = 2.0 * (hi - lo) * W * nq / (ms_per_step / 1000.0)
         roofline = {"bound": "popc", "achieved": pc_ach / 1e12, "peak": pc_peak / 1e12, "unit": "TPOPC32/s",
                     "frac": pc_ach / pc_peak, "traffic": None, "kernel": "scan_kernel",
-                    "peak_source": "tools/probe/ubench.cu POPC microbenchmark (16/clk/SM)"}
+                    "peak_source": "tools/probe/ubench.cu POPC microbenchmark (16/clk/SM)",
+                    "note": ("hybrid: %d of %d queries per step finished by the exhaustive scan; frac "
+                             "counts the scan's popcounts over the whole step" % (switched, nq))
+                    if args.method != "scan" else "exhaustive K6 path"}
     else:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak if peak else None, "traffic": None,
                     "kernel": "mih_probe_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                     "alg_bytes_per_step": alg_bytes, "probe_ms_per_step": probe_ms,
                     "probe_launches_per_step": probe_launches,
+                "hybrid_scan_queries_per_step": (prof1.switched_queries - prof0.switched_queries) / args.steps,
                     "step_frac_of_roofline": (alg_bytes / (ms_per_step / 1000.0) / 1e9) / peak,
                     "popc64_per_step": popc64,
                     "mean_trace": {"lookups": float(lookups.mean()), "candidates": float(cands.mean()),

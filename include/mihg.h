@@ -161,6 +161,7 @@ typedef struct mihg_profile {
   uint64_t probe_launches;
   double scan_ms;
   uint64_t scan_launches;
+  uint64_t switched_queries; /* untraced kNN queries finished by the exhaustive scan (hybrid) */
 } mihg_profile;
 int mihg_profile_enable(int on);
 void mihg_profile_reset(void);

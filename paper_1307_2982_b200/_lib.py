@@ -55,7 +55,7 @@ class TableInfo(C.Structure):
 class Profile(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("probe_ms", C.c_double),
                 ("probe_launches", C.c_uint64), ("scan_ms", C.c_double),
-                ("scan_launches", C.c_uint64)]
+                ("scan_launches", C.c_uint64), ("switched_queries", C.c_uint64)]
 
 
 # every symbol include/mihg.h declares: (name, restype, argtypes)

@@ -330,6 +330,7 @@ void mihg_profile_reset(void) {
   mihg::ProfileState& p = mihg::profile();
   p.probe_ms = p.scan_ms = 0;
   p.probe_launches = p.scan_launches = 0;
+  p.switched_queries = 0;
 }
 
 int mihg_profile_read(mihg_profile* out) {
@@ -339,6 +340,7 @@ int mihg_profile_read(mihg_profile* out) {
   out->probe_launches = p.probe_launches;
   out->scan_ms = p.scan_ms;
   out->scan_launches = p.scan_launches;
+  out->switched_queries = p.switched_queries;
   return MIHG_OK;
 }
 

@@ -190,6 +190,7 @@ struct ProfileState {
   uint64_t probe_launches = 0;
   double scan_ms = 0;
   uint64_t scan_launches = 0;
+  uint64_t switched_queries = 0;  // queries finished by the exhaustive scan (hybrid switch)
 };
 ProfileState& profile();  // thread-local message behind mihg_last_error()
 

@@ -816,6 +816,55 @@ uint32_t read_counter(const uint32_t* d, uint32_t* h, cudaStream_t st) {
   return *h;
 }
 
+// Hybrid switch: queries still active when the probe budget is exhausted are finished by the
+// exact exhaustive scan. Their MIH state is neutralised so finish/select skip them.
+__global__ void neutralise_kernel(const uint32_t* __restrict__ act, uint32_t nact, uint32_t* final_r,
+                                  uint32_t* bufcnt, uint32_t* dropmin) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nact; i += gridDim.x * blockDim.x) {
+    const uint32_t q = act[i];
+    final_r[q] = 0;
+    bufcnt[q] = 0;
+    dropmin[q] = 0xFFFFFFFFu;
+  }
+}
+
+__global__ void gather_rows_kernel(const uint64_t* __restrict__ src, const uint32_t* __restrict__ rows,
+                                   uint32_t nrows, uint32_t width, uint64_t* __restrict__ dst) {
+  const uint64_t total = uint64_t(nrows) * width;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = t / width;
+    dst[t] = src[uint64_t(rows[i]) * width + (t - i * width)];
+  }
+}
+
+__global__ void scatter_rows_kernel(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ dists,
+                                    const uint32_t* __restrict__ rows, uint32_t nrows, uint32_t k,
+                                    uint32_t* __restrict__ out_ids, uint32_t* __restrict__ out_dists) {
+  const uint64_t total = uint64_t(nrows) * k;
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = t / k;
+    out_ids[uint64_t(rows[i]) * k + (t - i * k)] = ids[t];
+    out_dists[uint64_t(rows[i]) * k + (t - i * k)] = dists[t];
+  }
+}
+
+// Cost of one more MIH round for each active query vs an exhaustive scan of that query, in
+// 64-bit popcount units (the scan costs n*W per query): one probe ~ 36 + 15*(W-1) units,
+// measured on B200 from the MIH probe rate vs the K6 scan rate (config 4, W=1: 36; config 5,
+// W=4: ~80). MIHG_HYBRID_ALPHA (default 0.5) scales the scan budget; MIHG_HYBRID=0 disables
+// the switch. Traced calls never switch (the trace is defined by the MIH probe sequence).
+double hybrid_alpha() {
+  static const double v = [] {
+    const char* h = std::getenv("MIHG_HYBRID");
+    if (h && h[0] == '0') return 0.0;
+    const char* e = std::getenv("MIHG_HYBRID_ALPHA");
+    return e ? std::atof(e) : 0.5;
+  }();
+  return v;
+}
+
 ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   ProbeArgs p{};
   p.codes = idx.codes.get();
@@ -924,11 +973,23 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   uint32_t* act_out = ws.act1.get();
   uint64_t nact = nq;
   uint64_t acc = 0;
+  const double alpha = d_tr ? 0.0 : hybrid_alpha();
+  const double scan_pairs = double(idx.n) * idx.W, probe_pairs = 36.0 + 15.0 * (idx.W - 1);
+  uint32_t* switched = nullptr;
+  uint64_t nswitched = 0;
   for (uint32_t r = 0; nact > 0; ++r) {
     if (r > idx.bits) throw CudaError("knn: radius loop exceeded the code width (internal error)");
     const uint32_t a = r % m, rr = r / m;
     const uint32_t s = idx.lengths[a];
     const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
+    if (alpha > 0 && double(acc + ring) * probe_pairs >= alpha * scan_pairs) {
+      switched = act_in;  // every active query has probed the same `acc` buckets so far
+      nswitched = nact;
+      neutralise_kernel<<<unsigned(std::min<uint64_t>((nact + 255) / 256, 1024)), 256, 0, st>>>(
+          act_in, uint32_t(nact), ws.final_r.get(), ws.bufcnt.get(), ws.dropmin.get());
+      MIHG_LAUNCH();
+      break;
+    }
     acc += ring;
     lookups_prefix.push_back(acc);
     if (ring) {
@@ -982,6 +1043,20 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   sa.out_ids = d_ids;
   sa.out_dists = d_dists;
   select_topk(sa, uint32_t(nq), st);
+
+  if (nswitched) {  // exhaustive K6 scan for the queries MIH would have spent longer on
+    DeviceBuffer<uint64_t> tq(nswitched * idx.W, st);
+    DeviceBuffer<uint32_t> ti(nswitched * k, st), td(nswitched * k, st);
+    const unsigned gg = unsigned(std::min<uint64_t>((nswitched * idx.W + 255) / 256, 4096));
+    gather_rows_kernel<<<gg, 256, 0, st>>>(d_q, switched, uint32_t(nswitched), idx.W, tq.get());
+    MIHG_LAUNCH();
+    scan_knn_device(idx.codes.get(), idx.n, idx.bits, idx.id_base, tq.get(), nswitched, k, ti.get(),
+                    td.get(), st);
+    scatter_rows_kernel<<<unsigned(std::min<uint64_t>((nswitched * k + 255) / 256, 4096)), 256, 0, st>>>(
+        ti.get(), td.get(), switched, uint32_t(nswitched), k, d_ids, d_dists);
+    MIHG_LAUNCH();
+    profile().switched_queries += nswitched;
+  }
 
   if (nre == 0) return;
   RerunResult rr_res = rerun_pass(idx, p, rerun.get(), nre, need.get(), nq, st);

@@ -50,6 +50,9 @@ def test_knn_matches_reference_golden(cuda_ok, golden, name, layout):
         assert np.array_equal(dists, d[f"dists_k{k}"]), (name, k)
         assert np.array_equal(ids, d[f"ids_k{k}"]), (name, k)
         assert np.array_equal(_trace_array(tr), d[f"trace_k{k}"]), (name, k)
+        # untraced calls may finish hard queries with the exhaustive scan (hybrid switch)
+        ids, dists = idx.knn_search_batch(d["queries"], k)
+        assert np.array_equal(ids, d[f"ids_k{k}"]) and np.array_equal(dists, d[f"dists_k{k}"]), (name, k)
 
 
 @pytest.mark.parametrize("bits", [64, 70])
@@ -225,6 +228,8 @@ def test_random_shapes_vs_oracle(cuda_ok, port, bits, m, n):
             ids, dists, tr = idx.knn_search_batch(qs, k, with_trace=True)
             oi, od = port.scan_knn(db.raw_words(), bits, qs, k)
             assert np.array_equal(ids, oi) and np.array_equal(dists, od), (layout, k)
+            ui, ud = idx.knn_search_batch(qs, k)  # untraced: hybrid MIH/scan
+            assert np.array_equal(ui, oi) and np.array_equal(ud, od), (layout, k)
             t = _trace_array(tr)
             assert np.array_equal(t[:, 4], od[:, -1]), "final_radius == d_k"
             assert np.array_equal(t, closed_form_traces(db.raw_words(), bits, m, qs, t[:, 4])), (layout, k)

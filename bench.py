@@ -50,7 +50,7 @@ MIX_DIM, MIX_COMPS = 128, 64
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -259,7 +259,8 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
-    if world > 1:
+    use_dist = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ  # torchrun: exchange path even at N=1
+    if use_dist:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -283,7 +284,7 @@ def main():
     kk = min(k, hi - lo)  # shard-local k (exact: global top-k is inside the union of local top-k)
     ids = torch.empty((nq, kk), dtype=torch.int32, device=dev)
     dists = torch.empty((nq, kk), dtype=torch.int32, device=dev)
-    if world > 1:
+    if use_dist:
         all_ids = torch.empty((world, nq, kk), dtype=torch.int32, device=dev)
         all_d = torch.empty((world, nq, kk), dtype=torch.int32, device=dev)
         out_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
@@ -297,7 +298,7 @@ def main():
         else:
             idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
                                   stream=stream.cuda_stream)
-        if world > 1:
+        if use_dist:
             dist.all_gather_into_tensor(all_ids, ids)
             dist.all_gather_into_tensor(all_d, dists)
             _lib.check(L.mihg_merge_topk_device(C.c_void_p(all_ids.data_ptr()), C.c_void_p(all_d.data_ptr()),
@@ -342,6 +343,24 @@ def main():
     probe_ms = prof1.probe_ms / args.steps
     probe_launches = prof1.probe_launches / args.steps
 
+    # ---- verify before reporting (tools/mih.cpp:274-301 pattern): MIH == exhaustive scan ----
+    nv = min(nq, 64)
+    vi = torch.empty((nv, kk), dtype=torch.int32, device=dev)
+    vd = torch.empty((nv, kk), dtype=torch.int32, device=dev)
+    si = torch.empty((nv, kk), dtype=torch.int32, device=dev)
+    sd = torch.empty((nv, kk), dtype=torch.int32, device=dev)
+    idx.knn_search_device(queries.data_ptr(), nv, kk, vi.data_ptr(), vd.data_ptr(), stream=stream.cuda_stream)
+    idx.scan_knn_device(queries.data_ptr(), nv, kk, si.data_ptr(), sd.data_ptr(), stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    verified = bool(torch.equal(vi, si) and torch.equal(vd, sd))
+    if use_dist:  # every shard checks its local result; all must pass
+        vt = torch.tensor([1 if verified else 0], device=dev)
+        dist.all_reduce(vt, op=dist.ReduceOp.MIN)
+        verified = bool(vt.item())
+    if not verified:
+        print(json.dumps({"error": "verification failed: MIH result differs from the exhaustive scan"}))
+        sys.exit(3)
+
     # ---- algorithmic bytes from the reference-identical traces (untimed run) ----
     tr = torch.empty((nq, 5), dtype=torch.int64, device=dev)
     idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(), tr.data_ptr(),
@@ -357,7 +376,7 @@ def main():
     hq = torch.from_numpy(np.ascontiguousarray(queries.cpu().numpy())).pin_memory()
     hid = torch.empty((nq, k), dtype=torch.int32).pin_memory()
     hd = torch.empty((nq, k), dtype=torch.int32).pin_memory()
-    if world == 1:
+    if not use_dist:
         def e2e_step():
             qp = C.cast(C.c_void_p(hq.data_ptr()), _lib.u64p)
             ip = C.cast(C.c_void_p(hid.data_ptr()), _lib.u32p)
@@ -464,7 +483,7 @@ def main():
             "data": "synthetic", "config": config_desc(cfg, args, world),
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(nq * W * 8),
                     "d2h_bytes_per_step": int(nq * k * 8)},
-            "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": launches, "verified_vs_scan": verified, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "setup": {"gen_s": gen_s, "index_build_s": build_s, "index_device_bytes": idx.device_bytes()},
         }
         print(json.dumps(line))

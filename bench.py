@@ -428,6 +428,14 @@ def main():
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    # DRAM traffic of the probe kernels per step, from a committed ncu capture of the same
+    # config (tools/ncu_traffic.sh; traffic is a profiler measurement, never taken live)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01", f"traffic_c{args.config}.json")
+    if os.path.exists(tp) and cfg["n"] == CONFIGS[args.config]["n"] and cfg["nq"] == CONFIGS[args.config]["nq"]:
+        tj = json.load(open(tp))
+        traffic = {"dram_bytes_per_step": tj["dram_bytes_per_step"], "over_alg_bytes": tj["traffic_over_alg"],
+                   "source": os.path.relpath(tp, ROOT)}
     achieved = alg_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else 0.0
     switched = (prof1.switched_queries - prof0.switched_queries) / args.steps
     if args.method == "scan" or switched >= 0.5 * nq:
@@ -443,7 +451,7 @@ def main():
                     if args.method != "scan" else "exhaustive K6 path"}
     else:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak if peak else None, "traffic": None,
+                    "frac": achieved / peak if peak else None, "traffic": traffic,
                     "kernel": "mih_probe_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                     "alg_bytes_per_step": alg_bytes, "probe_ms_per_step": probe_ms,
                     "probe_launches_per_step": probe_launches,

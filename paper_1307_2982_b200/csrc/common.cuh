@@ -86,6 +86,14 @@ constexpr int kBinomStride = 65;
 const uint64_t* device_binomials();  // [65][65] on the current device
 uint64_t host_binom(uint32_t n, uint32_t k);
 
+// One 256-bit global load (sm_100a LDG.E.ENL2.256): a whole directory block or 256-bit code.
+__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
+  asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "l"(p));
+}
+
 // ---- bucket probe: [lo, hi) slice of ids[] for bucket `v` (table.hpp:178-188 semantics).
 __device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint32_t& lo,
                                              uint32_t& hi) {
@@ -94,12 +102,12 @@ __device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint
     hi = __ldg(t.offsets + v + 1);
     return;
   }
-  const uint4* bp = reinterpret_cast<const uint4*>(t.dir + (v >> kDirBucketsLog2));
-  const uint4 x = __ldg(bp);
-  const uint4 y = __ldg(bp + 1);
+  uint32_t r[8];
+  ldg256(t.dir + (v >> kDirBucketsLog2), r);
+  const uint4 y = make_uint4(r[4], r[5], r[6], r[7]);
   const uint32_t tt = v & 63u;
-  const uint64_t p0 = (uint64_t(x.y) << 32) | x.x, p1 = (uint64_t(x.w) << 32) | x.z,
-                 p2 = (uint64_t(y.y) << 32) | y.x;
+  const uint64_t p0 = (uint64_t(r[1]) << 32) | r[0], p1 = (uint64_t(r[3]) << 32) | r[2],
+                 p2 = (uint64_t(r[5]) << 32) | r[4];
   const uint32_t c = uint32_t((p0 >> tt) & 1u) | (uint32_t((p1 >> tt) & 1u) << 1) |
                      (uint32_t((p2 >> tt) & 1u) << 2);
   if (c == 0) {
@@ -142,12 +150,10 @@ __device__ __forceinline__ void load_code(const uint64_t* __restrict__ codes, ui
     x[0] = v.x;
     x[1] = v.y;
   } else if constexpr (W == 4) {
-    const ulonglong2 v0 = __ldg(reinterpret_cast<const ulonglong2*>(p));
-    const ulonglong2 v1 = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
-    x[0] = v0.x;
-    x[1] = v0.y;
-    x[2] = v1.x;
-    x[3] = v1.y;
+    uint32_t r[8];
+    ldg256(p, r);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) x[w] = (uint64_t(r[2 * w + 1]) << 32) | r[2 * w];
   } else {
 #pragma unroll
     for (int w = 0; w < W; ++w) x[w] = __ldg(p + w);

@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=0, help="queries per CPU-reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="probe", choices=["probe", "id"],
+                    help="N>1: probe = every rank holds the index and probes 1/N of the substring key "
+                         "space (work divides by N); id = id-range shards (north_star's layout)")
     ap.add_argument("--method", default="mih", choices=["mih", "scan"],
                     help="mih: MihIndex::knn_search path (default); scan: the exhaustive K6 comparator")
     return ap.parse_args()
@@ -147,11 +150,21 @@ def make_codes_device(cfg, lo, hi, seed, torch, dev, lib):
         _lib.check(lib.mihg_gen_mixture_device(lo, n, cfg["bits"], MIX_DIM, MIX_COMPS, cfg["model_seed"],
                                                seed, C.c_void_p(out.data_ptr()), None))
         torch.cuda.synchronize(dev)
-    else:
-        host = np.zeros((max(n, 1), W), np.uint64)
+    else:  # mt19937_64 stream (gen_uniform), generated and uploaded in chunks
         from paper_1307_2982_b200 import _lib
-        _lib.check(lib.mihg_gen_uniform_range(lo, n, cfg["bits"], seed, host.ctypes.data_as(_lib.u64p)))
-        out.copy_(torch.from_numpy(host.view(np.int64)))
+        st = C.c_void_p()
+        _lib.check(lib.mihg_mt64_create(seed, C.byref(st)))
+        try:
+            _lib.check(lib.mihg_mt64_next_codes(st, lo, cfg["bits"], None))  # skip [0, lo)
+            chunk = 1 << 25
+            host = torch.empty((min(chunk, max(n, 1)), W), dtype=torch.int64).pin_memory()
+            for c0 in range(0, n, chunk):
+                cn = min(chunk, n - c0)
+                hv = host[:cn]
+                _lib.check(lib.mihg_mt64_next_codes(st, cn, cfg["bits"], C.cast(C.c_void_p(hv.data_ptr()), _lib.u64p)))
+                out[c0:c0 + cn].copy_(hv)
+        finally:
+            lib.mihg_mt64_free(st)
     return out
 
 
@@ -171,7 +184,10 @@ def config_desc(cfg, args, world):
     d = {"workload": f"BASELINE config {args.config}: exact {cfg['k']}-NN over n={cfg['n']:.0e} "
                      f"{cfg['bits']}-bit {cfg['data']} codes, {cfg['nq']} queries, MIH m={cfg['m']}",
          "n": cfg["n"], "bits": cfg["bits"], "m": cfg["m"], "k": cfg["k"], "queries": cfg["nq"],
-         "data_generator": cfg["data"], "parallelism": f"id-range shards x{world}",
+         "data_generator": cfg["data"],
+         "parallelism": (f"probe-space partition x{world} (replicated index, 1/{world} of the key space "
+                         f"per rank, per-round NCCL histogram all-reduce)" if world > 1 and args.shard == "probe"
+                         else f"id-range shards x{world}"),
          "l2_policy": "inputs larger than L2 (index >> 126 MB); no flush"}
     if cfg["data"] == "mixture":
         d.update({"mixture": {"dim": MIX_DIM, "components": MIX_COMPS, "sigma_rel": 1.0,
@@ -266,7 +282,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     L = _lib.lib()
     bits, m, k, nq, W = cfg["bits"], cfg["m"], cfg["k"], cfg["nq"], wpc(cfg["bits"])
-    lo, hi = shard_range(cfg["n"], rank, world)
+    probe_part = world > 1 and args.shard == "probe" and args.method == "mih"
+    lo, hi = (0, cfg["n"]) if probe_part else shard_range(cfg["n"], rank, world)
 
     # ---- data + index (setup, untimed) ----
     t0 = time.time()
@@ -291,13 +308,19 @@ def main():
         out_d = torch.empty((nq, k), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    partition = None
+    if probe_part:
+        from paper_1307_2982_b200.shard import nccl_allreduce
+
+        partition = (world, rank, nccl_allreduce())
+
+    def step(qptr=None):
+        qptr = qptr or queries.data_ptr()
         if args.method == "scan":
-            idx.scan_knn_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
-                                stream=stream.cuda_stream)
+            idx.scan_knn_device(qptr, nq, kk, ids.data_ptr(), dists.data_ptr(), stream=stream.cuda_stream)
         else:
-            idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
-                                  stream=stream.cuda_stream)
+            idx.knn_search_device(qptr, nq, kk, ids.data_ptr(), dists.data_ptr(),
+                                  stream=stream.cuda_stream, partition=partition)
         if use_dist:
             dist.all_gather_into_tensor(all_ids, ids)
             dist.all_gather_into_tensor(all_d, dists)
@@ -349,10 +372,15 @@ def main():
     vd = torch.empty((nv, kk), dtype=torch.int32, device=dev)
     si = torch.empty((nv, kk), dtype=torch.int32, device=dev)
     sd = torch.empty((nv, kk), dtype=torch.int32, device=dev)
-    idx.knn_search_device(queries.data_ptr(), nv, kk, vi.data_ptr(), vd.data_ptr(), stream=stream.cuda_stream)
-    idx.scan_knn_device(queries.data_ptr(), nv, kk, si.data_ptr(), sd.data_ptr(), stream=stream.cuda_stream)
-    torch.cuda.synchronize(dev)
-    verified = bool(torch.equal(vi, si) and torch.equal(vd, sd))
+    if probe_part:  # merged output of the last timed step (first nv rows) vs a full-index scan
+        idx.scan_knn_device(queries.data_ptr(), nv, k, si.data_ptr(), sd.data_ptr(), stream=stream.cuda_stream)
+        torch.cuda.synchronize(dev)
+        verified = bool(torch.equal(out_ids[:nv], si) and torch.equal(out_d[:nv], sd))
+    else:
+        idx.knn_search_device(queries.data_ptr(), nv, kk, vi.data_ptr(), vd.data_ptr(), stream=stream.cuda_stream)
+        idx.scan_knn_device(queries.data_ptr(), nv, kk, si.data_ptr(), sd.data_ptr(), stream=stream.cuda_stream)
+        torch.cuda.synchronize(dev)
+        verified = bool(torch.equal(vi, si) and torch.equal(vd, sd))
     if use_dist:  # every shard checks its local result; all must pass
         vt = torch.tensor([1 if verified else 0], device=dev)
         dist.all_reduce(vt, op=dist.ReduceOp.MIN)
@@ -364,7 +392,7 @@ def main():
     # ---- algorithmic bytes from the reference-identical traces (untimed run) ----
     tr = torch.empty((nq, 5), dtype=torch.int64, device=dev)
     idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(), tr.data_ptr(),
-                          stream=stream.cuda_stream)
+                          stream=stream.cuda_stream, partition=partition)
     torch.cuda.synchronize(dev)
     t = tr.cpu().numpy()
     lookups, cands, uniq, radius = (t[:, 0].astype(np.float64), t[:, 1].astype(np.float64),
@@ -390,17 +418,7 @@ def main():
 
         def e2e_step():
             dq.copy_(hq, non_blocking=True)
-            if args.method == "scan":
-                idx.scan_knn_device(dq.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
-                                    stream=stream.cuda_stream)
-            else:
-                idx.knn_search_device(dq.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(),
-                                      stream=stream.cuda_stream)
-            dist.all_gather_into_tensor(all_ids, ids)
-            dist.all_gather_into_tensor(all_d, dists)
-            _lib.check(L.mihg_merge_topk_device(C.c_void_p(all_ids.data_ptr()), C.c_void_p(all_d.data_ptr()),
-                                                world, nq, kk, k, C.c_void_p(out_ids.data_ptr()),
-                                                C.c_void_p(out_d.data_ptr()), C.c_void_p(stream.cuda_stream)))
+            step(dq.data_ptr())
             hid.copy_(out_ids, non_blocking=True)
             hd.copy_(out_d, non_blocking=True)
             torch.cuda.synchronize(dev)
@@ -432,11 +450,13 @@ def main():
     # config (tools/ncu_traffic.sh; traffic is a profiler measurement, never taken live)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "r01", f"traffic_c{args.config}.json")
-    if os.path.exists(tp) and cfg["n"] == CONFIGS[args.config]["n"] and cfg["nq"] == CONFIGS[args.config]["nq"]:
+    if (os.path.exists(tp) and world == 1 and cfg["n"] == CONFIGS[args.config]["n"]
+            and cfg["nq"] == CONFIGS[args.config]["nq"]):
         tj = json.load(open(tp))
         traffic = {"dram_bytes_per_step": tj["dram_bytes_per_step"], "over_alg_bytes": tj["traffic_over_alg"],
                    "source": os.path.relpath(tp, ROOT)}
-    achieved = alg_bytes / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else 0.0
+    # per GPU: a probe-partitioned rank moves 1/N of the step's algorithmic bytes
+    achieved = alg_bytes / (world if probe_part else 1) / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else 0.0
     switched = (prof1.switched_queries - prof0.switched_queries) / args.steps
     if args.method == "scan" or switched >= 0.5 * nq:
         # K6 is POPC-bound: n*W popc64 = 2*n*W POPC32 per query; peak = 16 POPC/clk/SM measured

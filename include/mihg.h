@@ -132,6 +132,25 @@ int mihg_range_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint
                      uint64_t* out_offsets, uint32_t* out_ids, uint32_t* out_dists, uint64_t capacity,
                      mihg_trace* traces);
 
+/* Probe-space partitioned kNN for multi-GPU (SURVEY.md §8e remedy (iii)): every rank holds the
+ * same index; rank `rank` of `count` (power of two) probes only ring values whose top
+ * log2(count) substring bits equal `rank`, so probe AND verification work divide by count.
+ * `allreduce(user, dev_ptr, n, dtype, stream)` must sum n device elements (dtype 0: u32,
+ * 1: u64) in place across ranks, ordered on `stream`, and return 0 (e.g. an NCCL all-reduce);
+ * it is called once per radius round with the per-query histograms, so all ranks apply the
+ * reference's stopping rule to the global counts. Outputs are the rank's LOCAL top-k (padded
+ * with 0xFFFFFFFF): all-gather them and merge with mihg_merge_topk_device. Traces are global. */
+typedef int (*mihg_allreduce_fn)(void* user, void* dev_ptr, uint64_t count, int dtype, void* stream);
+typedef struct mihg_partition {
+  uint32_t count;
+  uint32_t rank;
+  mihg_allreduce_fn allreduce;
+  void* user;
+} mihg_partition;
+int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
+                               uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces,
+                               const mihg_partition* part, void* stream);
+
 /* scan_knn(db, q, k) — scan.hpp:43-68, batched, over the index's device codes. */
 int mihg_scan_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,
                         uint32_t* out_ids, uint32_t* out_dists);
@@ -152,6 +171,13 @@ int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint3
 int mihg_gen_uniform(uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out);
 /* Codes [first, first + n) of gen_uniform(., bits, seed) — an id-range shard of the same stream. */
 int mihg_gen_uniform_range(uint64_t first, uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out);
+
+/* Streaming gen_uniform: the same mt19937_64 sequence produced chunk by chunk (out == NULL
+ * skips codes), so large databases are generated without holding them on the host. */
+typedef struct mihg_mt64 mihg_mt64;
+int mihg_mt64_create(uint64_t seed, mihg_mt64** out);
+int mihg_mt64_next_codes(mihg_mt64* state, uint64_t n, uint32_t bits, uint64_t* out);
+void mihg_mt64_free(mihg_mt64* state);
 
 /* Live profiling: kernel launch count of this library (process-wide), and CUDA-event time of the
  * MIH probe kernel launches (recorded on their own stream) while enabled. */

@@ -52,6 +52,16 @@ class TableInfo(C.Structure):
                 ("escaped_blocks", C.c_uint64)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p)
+
+
+class Partition(C.Structure):
+    """mihg_partition: probe-space partition of a multi-GPU kNN call."""
+
+    _fields_ = [("count", C.c_uint32), ("rank", C.c_uint32), ("allreduce", ALLREDUCE_FN),
+                ("user", C.c_void_p)]
+
+
 class Profile(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("probe_ms", C.c_double),
                 ("probe_launches", C.c_uint64), ("scan_ms", C.c_double),
@@ -77,6 +87,9 @@ SYMBOLS = [
                                         C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mihg_range_batch", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint32, u64p, u32p, u32p,
                                    C.c_uint64, C.POINTER(Trace)]),
+    ("mihg_knn_batch_device_part", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
+                                             C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.POINTER(Partition), C.c_void_p]),
     ("mihg_scan_knn_batch", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint32, u32p, u32p]),
     ("mihg_scan_knn_batch_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                              C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -87,6 +100,9 @@ SYMBOLS = [
                                          C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
     ("mihg_gen_uniform", C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, u64p]),
+    ("mihg_mt64_create", C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("mihg_mt64_next_codes", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, u64p]),
+    ("mihg_mt64_free", None, [C.c_void_p]),
     ("mihg_gen_uniform_range", C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, u64p]),
     ("mihg_gen_mixture_device", C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                                           C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p,

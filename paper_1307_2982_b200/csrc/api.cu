@@ -233,6 +233,27 @@ int mihg_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t n
   });
 }
 
+int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
+                               uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces,
+                               const mihg_partition* part, void* stream) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    mihg::Partition pt;
+    if (part) {
+      pt.count = part->count;
+      pt.rank = part->rank;
+      pt.allreduce = part->allreduce;
+      pt.user = part->user;
+    }
+    mihg::KnnOptions opt;
+    opt.part = part ? &pt : nullptr;
+    mihg::knn_device(ix, d_queries, nq, k, d_ids, d_dists, reinterpret_cast<mihg::Trace*>(d_traces),
+                     static_cast<cudaStream_t>(stream), opt);
+  });
+}
+
 int mihg_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,
                    uint32_t* out_ids, uint32_t* out_dists, mihg_trace* traces) {
   return guarded([&] {
@@ -342,6 +363,33 @@ int mihg_profile_read(mihg_profile* out) {
   out->scan_launches = p.scan_launches;
   out->switched_queries = p.switched_queries;
   return MIHG_OK;
+}
+
+struct mihg_mt64 {
+  Mt64 g;
+  explicit mihg_mt64(uint64_t seed) : g(seed) {}
+};
+
+int mihg_mt64_create(uint64_t seed, mihg_mt64** out) {
+  return guarded([&] { *out = new mihg_mt64(seed); });
+}
+
+void mihg_mt64_free(mihg_mt64* s) { delete s; }
+
+int mihg_mt64_next_codes(mihg_mt64* s, uint64_t n, uint32_t bits, uint64_t* out) {
+  return guarded([&] {
+    if (bits == 0 || bits > mihg::kMaxCodeBits) throw mihg::InvalidArgument("gen_uniform: bad width");
+    const uint32_t wpc = mihg::words_per_code(bits);
+    const uint64_t mask = (bits & 63) == 0 ? ~uint64_t(0) : ((uint64_t(1) << (bits & 63)) - 1);
+    for (uint64_t i = 0; i < n; ++i) {
+      uint64_t* w = out ? out + i * wpc : nullptr;
+      for (uint32_t k = 0; k < wpc; ++k) {
+        const uint64_t v = s->g();
+        if (w) w[k] = v;
+      }
+      if (w) w[wpc - 1] &= mask;
+    }
+  });
 }
 
 int mihg_gen_uniform(uint64_t n, uint32_t bits, uint64_t seed, uint64_t* out) {

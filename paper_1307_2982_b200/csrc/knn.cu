@@ -41,6 +41,7 @@ struct Workspace {
   uint64_t nq_cap = 0;
   uint32_t b1 = 0, m = 0, cap = 0;
   DeviceBuffer<uint64_t> qcodes_pad;
+  DeviceBuffer<uint32_t> hist_g;  // all-reduced histograms (partitioned calls)
   DeviceBuffer<uint32_t> qsub, hist, ubound, bufcnt, dropmin, act0, act1, counters, final_r;
   DeviceBuffer<uint64_t> buf;
   DeviceBuffer<unsigned long long> trc;
@@ -207,6 +208,7 @@ struct ProbeArgs {
   // L2-sliced rounds (slice_bits > 0): active queries grouped by the top t bits G of their
   // substring; units enumerated per (slice P, group G) pair, P-major, claimed in order.
   uint32_t slice_bits;
+  uint32_t part_bits, part_id;  // probe-space partition (multi-GPU): top key bits owned
   const uint64_t* pair_prefix;  // 4^t + 1 exclusive unit prefix over (P, G) pairs
   const uint32_t* gstart;       // 2^t + 1 group starts into grouped[]
   const uint32_t* grouped;      // active slots sorted by group
@@ -254,7 +256,8 @@ __global__ void __launch_bounds__(1024) slice_plan_kernel(ProbeArgs p, uint32_t 
     if (idx >= npairs) break;
     const uint32_t P = idx >> t, g = idx & (G - 1), h = __popc(P ^ g);
     uint64_t c = 0;
-    if (h <= p.rr && p.rr - h <= sb)
+    const bool owned = p.part_bits == 0 || (P >> (t - p.part_bits)) == p.part_id;
+    if (owned && h <= p.rr && p.rr - h <= sb)
       c = uint64_t(hist[g]) * ((p.binom[sb * kBinomStride + (p.rr - h)] + span - 1) / span);
     pair_prefix[idx] = c;  // temporarily the count
     run += c;
@@ -446,7 +449,8 @@ __global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kerne
       for (int b = 0; b < kLaneProbes; ++b) {
         uint32_t l = 0, h = 0;
         if (i < iend && it + b < p.chunk) {
-          probe_bucket(p.tab, qa ^ uint32_t(high | mask), l, h);
+          const uint32_t v = qa ^ uint32_t(high | mask);
+          if (p.part_bits == 0 || (v >> (p.tab.s - p.part_bits)) == p.part_id) probe_bucket(p.tab, v, l, h);
           mask = next_comb(mask);
           ++i;
         }
@@ -755,6 +759,7 @@ void plan_slicing(ProbeArgs& p, Workspace& ws, uint64_t nact, cudaStream_t st) {
   if (!slicing_enabled() || bytes <= 64.0 * (1 << 20) || double(nact) * double(p.ring) < 4.0e6) return;
   uint32_t t = 0;
   while (bytes / double(1u << t) > slice_mb() * (1 << 20) && t < 8) ++t;
+  t = std::max<uint32_t>(t, p.part_bits);  // slices nest inside the rank's key range
   t = std::min<uint32_t>(t, s - 1);
   if (t == 0) return;
   // the in-flight wavefront may span `inflight` slices (~half of L2): units per slice >=
@@ -954,8 +959,15 @@ RerunResult rerun_pass(Index& idx, const ProbeArgs& p, const uint32_t* d_rerun, 
   return res;
 }
 
+void call_allreduce(const Partition* part, void* ptr, uint64_t count, int dtype, cudaStream_t st) {
+  if (!part->allreduce) throw InvalidArgument("partitioned knn: no all-reduce callback");
+  const int rc = part->allreduce(part->user, ptr, count, dtype, st);
+  if (rc) throw CudaError("partitioned knn: all-reduce callback failed (" + std::to_string(rc) + ")");
+}
+
 void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_t* d_ids,
                uint32_t* d_dists, Trace* d_tr, cudaStream_t st, const KnnOptions& opt) {
+  const Partition* part = opt.part && opt.part->count > 1 ? opt.part : nullptr;
   Workspace& ws = *idx.ws;
   const uint32_t m = idx.m, b1 = idx.bits + 1, cap = ws.cap;
   const unsigned g1 = unsigned(std::min<uint64_t>((nq + 255) / 256, 4096));
@@ -967,13 +979,28 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   MIHG_LAUNCH();
 
   ProbeArgs p = make_probe_args(idx, ws, d_q);
+  uint64_t part_lo = 0, part_hi = idx.n;  // id range this rank scans if queries switch to K6
+  if (part) {
+    uint32_t bits = 0;
+    while ((1u << bits) < part->count) ++bits;
+    if ((1u << bits) != part->count || part->rank >= part->count)
+      throw InvalidArgument("partitioned knn: count must be a power of two and rank < count");
+    for (uint32_t j = 0; j < m; ++j)
+      if (idx.lengths[j] < bits) throw InvalidArgument("partitioned knn: substring narrower than log2(count)");
+    p.part_bits = bits;
+    p.part_id = part->rank;
+    if (ws.hist_g.size() < nq * b1) ws.hist_g = DeviceBuffer<uint32_t>(ws.nq_cap * b1, st);
+    const uint64_t per = (idx.n + part->count - 1) / part->count;
+    part_lo = std::min<uint64_t>(idx.n, uint64_t(part->rank) * per);
+    part_hi = std::min<uint64_t>(idx.n, part_lo + per);
+  }
 
   std::vector<uint64_t> lookups_prefix;
   uint32_t* act_in = ws.act0.get();
   uint32_t* act_out = ws.act1.get();
   uint64_t nact = nq;
   uint64_t acc = 0;
-  const double alpha = d_tr ? 0.0 : hybrid_alpha();
+  const double alpha = (d_tr || (part && part_hi - part_lo < k)) ? 0.0 : hybrid_alpha();
   const double scan_pairs = double(idx.n) * idx.W, probe_pairs = 36.0 + 15.0 * (idx.W - 1);
   uint32_t* switched = nullptr;
   uint64_t nswitched = 0;
@@ -1006,10 +1033,16 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
       dispatch_probe(p, d_tr != nullptr, st);
       if (prof.enabled) MIHG_CUDA(cudaEventRecord(ws.ev1, st));
     }
+    const uint32_t* hist_end = ws.hist.get();
+    if (part) {  // global histograms: every rank takes the same stopping / bound decision
+      MIHG_CUDA(cudaMemcpyAsync(ws.hist_g.get(), ws.hist.get(), nq * b1 * 4, cudaMemcpyDeviceToDevice, st));
+      call_allreduce(part, ws.hist_g.get(), nq * b1, 0, st);
+      hist_end = ws.hist_g.get();
+    }
     MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
     const unsigned g = unsigned((nact * 32 + 255) / 256);
     mih_round_end_kernel<<<g, 256, 0, st>>>(act_in, uint32_t(nact), act_out, ws.counters.get(),
-                                             ws.hist.get(), b1, ws.ubound.get(), k, r,
+                                             hist_end, b1, ws.ubound.get(), k, r,
                                              ws.final_r.get(), ws.bufcnt.get(), ws.buf.get(), cap);
     MIHG_LAUNCH();
     nact = read_counter(ws.counters.get(), ws.h_counter, st);  // synchronizes the stream
@@ -1023,6 +1056,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   }
   MIHG_CUDA(cudaMemcpyAsync(ws.lookups_prefix.get(), lookups_prefix.data(),
                             lookups_prefix.size() * 8, cudaMemcpyHostToDevice, st));
+  if (part && d_tr) call_allreduce(part, ws.trc.get(), 2 * nq, 1, st);  // global candidates/unique
   DeviceBuffer<uint32_t> seg_count(nq, st), need(nq, st), rerun(nq, st);
   MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
   mih_finish_kernel<<<g1, 256, 0, st>>>(nq, ws.final_r.get(), ws.hist.get(), b1, ws.bufcnt.get(),
@@ -1050,8 +1084,8 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     const unsigned gg = unsigned(std::min<uint64_t>((nswitched * idx.W + 255) / 256, 4096));
     gather_rows_kernel<<<gg, 256, 0, st>>>(d_q, switched, uint32_t(nswitched), idx.W, tq.get());
     MIHG_LAUNCH();
-    scan_knn_device(idx.codes.get(), idx.n, idx.bits, idx.id_base, tq.get(), nswitched, k, ti.get(),
-                    td.get(), st);
+    scan_knn_device(idx.codes.get() + part_lo * idx.W, part_hi - part_lo, idx.bits,
+                    idx.id_base + uint32_t(part_lo), tq.get(), nswitched, k, ti.get(), td.get(), st);
     scatter_rows_kernel<<<unsigned(std::min<uint64_t>((nswitched * k + 255) / 256, 4096)), 256, 0, st>>>(
         ti.get(), td.get(), switched, uint32_t(nswitched), k, d_ids, d_dists);
     MIHG_LAUNCH();
@@ -1106,7 +1140,7 @@ void knn_device(Index& idx, const uint64_t* d_queries, uint64_t nq, uint32_t k, 
   const uint64_t chunk = std::min<uint64_t>(nq, opt.query_chunk);
   const uint32_t cap = std::max<uint32_t>(opt.buffer_cap, 2 * k + 64);
   ensure_workspace(idx, chunk, cap, st);
-  for (uint64_t q0 = 0; q0 < nq; q0 += chunk) {
+  for (uint64_t q0 = 0; q0 < nq; q0 += chunk) {  // (partitioned: every rank runs the same chunks)
     const uint64_t cn = std::min(chunk, nq - q0);
     knn_chunk(idx, d_queries + q0 * idx.W, cn, k, d_ids + q0 * k, d_dists + q0 * k,
               d_traces ? d_traces + q0 : nullptr, st, opt);

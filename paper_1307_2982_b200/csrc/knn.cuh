@@ -10,9 +10,21 @@ struct Trace {
 };
 static_assert(sizeof(Trace) == 40, "mihg_trace ABI");
 
+// Probe-space partition across ranks (multi-GPU): rank `rank` of `count` (a power of two) probes
+// only the ring values whose top log2(count) key bits equal `rank`; the per-query histograms are
+// summed across ranks every round through `allreduce` (in place on device memory, ordered on
+// `stream`; dtype 0 = u32, 1 = u64) so all ranks share the reference's stopping rule. The call
+// then returns the rank's LOCAL top-k candidates; the caller all-gathers and merges them.
+struct Partition {
+  uint32_t count = 1, rank = 0;
+  int (*allreduce)(void* user, void* dev_ptr, uint64_t count, int dtype, void* stream) = nullptr;
+  void* user = nullptr;
+};
+
 struct KnnOptions {
   uint32_t buffer_cap = 8192;   // per-query candidate buffer (u64 keys) in the main pass
   uint32_t query_chunk = 16384; // queries per workspace pass
+  const Partition* part = nullptr;
 };
 
 // Batched MihIndex::knn_search (index.hpp:185-253). All pointers are device pointers on

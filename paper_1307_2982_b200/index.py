@@ -239,12 +239,37 @@ class MihIndex:
         return (ids, dists, tr) if with_trace else (ids, dists)
 
     def knn_search_device(self, d_queries, nq: int, k: int, d_ids, d_dists, d_traces=None,
-                          stream: int = 0) -> None:
-        """Device-pointer batch (ints from torch .data_ptr()); ordered on `stream`."""
-        _lib.check(_lib.lib().mihg_knn_batch_device(self._h, C.c_void_p(d_queries), nq, k,
-                                                    C.c_void_p(d_ids), C.c_void_p(d_dists),
-                                                    C.c_void_p(d_traces) if d_traces else None,
-                                                    C.c_void_p(stream) if stream else None))
+                          stream: int = 0, partition=None) -> None:
+        """Device-pointer batch (ints from torch .data_ptr()); ordered on `stream`.
+
+        partition=(count, rank, allreduce) runs the probe-space partitioned search of one rank:
+        ``allreduce(dev_ptr, n, dtype, stream)`` sums n device elements (dtype 0 u32, 1 u64) in
+        place across ranks; the outputs are this rank's local top-k (merge across ranks)."""
+        L = _lib.lib()
+        sp = C.c_void_p(stream) if stream else None
+        tr = C.c_void_p(d_traces) if d_traces else None
+        if partition is None:
+            _lib.check(L.mihg_knn_batch_device(self._h, C.c_void_p(d_queries), nq, k, C.c_void_p(d_ids),
+                                               C.c_void_p(d_dists), tr, sp))
+            return
+        count, rank, fn = partition
+        errors = []
+
+        def _cb(user, ptr, n, dtype, strm):
+            try:
+                fn(int(ptr), int(n), int(dtype), int(strm or 0))
+                return 0
+            except Exception as e:  # surfaced after the call returns
+                errors.append(e)
+                return 1
+
+        cb = _lib.ALLREDUCE_FN(_cb)
+        part = _lib.Partition(count, rank, cb, None)
+        rc = L.mihg_knn_batch_device_part(self._h, C.c_void_p(d_queries), nq, k, C.c_void_p(d_ids),
+                                          C.c_void_p(d_dists), tr, C.byref(part), sp)
+        if errors:
+            raise errors[0]
+        _lib.check(rc)
 
     def range_search(self, q: BinaryCode, r: int, trace: SearchTrace | None = None, scratch=None):
         """index.hpp:149-176: exactly {(i, d_i) : d_i <= r}, sorted by (distance, id)."""

@@ -26,6 +26,36 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return lo, min(n, lo + per)
 
 
+class _CudaArray:
+    """Zero-copy view of raw device memory for torch (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def nccl_allreduce(group=None):
+    """Callback for MihIndex.knn_search_device(partition=...): in-place SUM over the group of a
+    device buffer (u32 counts as int32, u64 as int64), ordered on the library's stream."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(ptr: int, n: int, dtype: int, stream: int):
+        t = torch.as_tensor(_CudaArray(ptr, n, "<i4" if dtype == 0 else "<i8"), device="cuda")
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream)) if stream else _nullctx():
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    return fn
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def gpu_merge(all_ids, all_dists, k: int):
     """Exact k-way merge on the GPU: all_* are int32 CUDA tensors [G, nq, k_in]."""
     import torch
@@ -55,6 +85,29 @@ class ShardedKnn:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.merge = merge or gpu_merge
+
+    @classmethod
+    def probe_partitioned(cls, index, group=None):
+        """Every rank holds the full index and probes only its slice of the substring key
+        space (rank = top log2(G) key bits); per-round histograms are all-reduced over NCCL so
+        all ranks stop together, and the local top-k lists merge exactly. Divides probe and
+        verification work by G (id-range shards cannot: SURVEY.md §7 hard part 5)."""
+        import torch
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        ar = nccl_allreduce(group)
+
+        def local(queries, k):
+            nq = queries.shape[0]
+            ids = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
+            d = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
+            index.knn_search_device(queries.data_ptr(), nq, k, ids.data_ptr(), d.data_ptr(),
+                                    stream=torch.cuda.current_stream(queries.device).cuda_stream,
+                                    partition=(world, rank, ar) if world > 1 else None)
+            return ids, d
+
+        return cls(local, index.size(), group)
 
     @classmethod
     def from_index(cls, index, group=None):

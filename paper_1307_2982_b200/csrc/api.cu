@@ -1,4 +1,5 @@
 // C ABI (include/mihg.h) over the device index and kernels. No C++ exception crosses it.
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -107,6 +108,7 @@ int mihg_index_build_ex(const mihg_build_params* p, mihg_index** out) {
     mihg::BuildOptions opt;
     if (p->dense_max_bits) opt.dense_max_bits = p->dense_max_bits;
     opt.force = p->layout;
+    if (const char* e = std::getenv("MIHG_OCC")) opt.occupancy = e[0] == '1';  // A/B switch
     DeviceGuard g(p->device);
     mihg::Index* ix = mihg::build_index(p->codes, p->codes_on_device != 0, p->n, p->bits, p->m,
                                         p->lengths, p->positions, p->device, p->id_base, opt);

@@ -123,6 +123,14 @@ __global__ void gather_codes_kernel(const uint64_t* __restrict__ codes, uint32_t
   }
 }
 
+__global__ void occupancy_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ occ) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) atomicOr(occ + (k >> 5), 1u << (k & 31));  // first of its bucket
+  }
+}
+
 __global__ void bucket_hist_kernel(const uint32_t* __restrict__ keys, uint64_t n,
                                    uint32_t* __restrict__ cnt) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
@@ -284,6 +292,15 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
     MIHG_CUDA(cudaMemcpyAsync(&last_flag, flags.get() + nblocks - 1, 4, cudaMemcpyDeviceToHost, st));
     MIHG_CUDA(cudaStreamSynchronize(st));
     t->escaped_blocks = uint64_t(last_idx) + last_flag;
+    if (opt.occupancy && s >= 20) {  // 2^s bits; 512 MB for a 32-bit table
+      const uint64_t words = nb / 32;
+      t->occ = DeviceBuffer<uint32_t>(words, st);
+      MIHG_CUDA(cudaMemsetAsync(t->occ.get(), 0, words * 4, st));
+      if (n) {
+        occupancy_kernel<<<grid_for(n, 256), 256, 0, st>>>(keys.get(), n, t->occ.get());
+        MIHG_LAUNCH();
+      }
+    }
     if (t->escaped_blocks) {
       t->esc = DeviceBuffer<uint32_t>(t->escaped_blocks * 65, st);
       dir_build_kernel<1><<<grid, 256, 0, st>>>(keys.get(), n, nblocks, t->dir.get(), flags.get(),

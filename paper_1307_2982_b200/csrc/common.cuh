@@ -68,6 +68,7 @@ struct DevTable {
   const DirBlock* dir;      // sparse: 2^(s-6) blocks (nullptr when dense)
   const uint32_t* esc;      // sparse: 65 absolute starts per escaped block
   const uint64_t* codes;    // inline codes in table order (W words per entry), or nullptr
+  const uint32_t* occ;      // sparse: 1 bit per bucket (non-empty), or nullptr
   uint32_t s;
   uint32_t dense;
 };
@@ -100,6 +101,10 @@ __device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint
   if (t.dense) {
     lo = __ldg(t.offsets + v);
     hi = __ldg(t.offsets + v + 1);
+    return;
+  }
+  if (t.occ && !((__ldg(t.occ + (v >> 5)) >> (v & 31)) & 1u)) {  // empty: an L2 hit, no sector
+    lo = hi = 0;
     return;
   }
   uint32_t r[8];

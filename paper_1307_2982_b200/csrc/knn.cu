@@ -76,6 +76,7 @@ Index::~Index() {
       t->dir.reset();
       t->esc.reset();
       t->tcodes.reset();
+      t->occ.reset();
     }
   d_tables.reset();
   if (stream) {

@@ -12,6 +12,8 @@
  *   MIHG_ENOMEM   3  <-> std::bad_alloc (table.hpp:59)
  *   MIHG_ECUDA    4  CUDA runtime / kernel failure
  *   MIHG_ENCCL    5  (reserved for the multi-GPU layer; the C++/Python hosts raise it)
+ *   MIHG_EFORMAT  6  <-> FormatError (io.hpp:35-44), message carries the byte offset
+ *   MIHG_EIO      7  file open / read / write failure
  *
  * mihg_last_error() returns a thread-local message for the last failing call on this thread.
  *
@@ -38,6 +40,8 @@ extern "C" {
 #define MIHG_ENOMEM 3
 #define MIHG_ECUDA 4
 #define MIHG_ENCCL 5
+#define MIHG_EFORMAT 6  /* <-> FormatError (io.hpp:35-44); message ends "(byte offset N)" */
+#define MIHG_EIO 7      /* cannot open / read / write a file (std::runtime_error in io.hpp) */
 
 #define MIHG_ABI_VERSION 1
 
@@ -109,6 +113,13 @@ int mihg_table_get_info(const mihg_index* idx, uint32_t j, mihg_table_info* out)
  * insertion (ascending id) order; writes min(count, cap) ids (global ids). */
 int mihg_bucket_lookup(const mihg_index* idx, uint32_t j, uint64_t value, uint32_t* out_ids,
                        uint64_t cap, uint64_t* count);
+
+/* write_index(idx, path) — io.hpp:335-358: the BMIX index file, byte-identical to the
+ * reference's output for the same codes and partition. */
+int mihg_index_write(mihg_index* idx, const char* path);
+/* read_index(path) — io.hpp:360-425: parses and validates a BMIX file (reference checks and
+ * messages, MIHG_EFORMAT with byte offset) and loads the file's tables onto `device` as given. */
+int mihg_index_read(const char* path, int device, mihg_index** out);
 
 /* Device pointer to the index's codes (n * ceil(bits/64) words). */
 int mihg_index_codes(const mihg_index* idx, const uint64_t** d_codes);

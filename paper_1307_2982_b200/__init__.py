@@ -8,11 +8,11 @@ from .codes import (BinaryCode, CodeDatabase, Partition, consecutive_partition, 
                     hamming_distance, kMaxCodeBits, words_per_code)
 from .index import (MihIndex, Neighbor, SearchTrace, TableStats, build_index, neighbor_less,
                     scan_knn)
-from .io import FormatError, gen_uniform, read_codes, write_codes
+from .io import FormatError, gen_uniform, read_codes, read_index, write_codes, write_index
 
 __all__ = [
     "BinaryCode", "CodeDatabase", "Partition", "consecutive_partition", "extract_substring",
     "hamming_distance", "kMaxCodeBits", "words_per_code", "MihIndex", "Neighbor", "SearchTrace",
     "TableStats", "build_index", "neighbor_less", "scan_knn", "FormatError", "gen_uniform",
-    "read_codes", "write_codes",
+    "read_codes", "write_codes", "read_index", "write_index",
 ]

@@ -11,7 +11,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmihg.so")
 
-MIHG_OK, MIHG_EINVAL, MIHG_EINTERNAL, MIHG_ENOMEM, MIHG_ECUDA, MIHG_ENCCL = range(6)
+MIHG_OK, MIHG_EINVAL, MIHG_EINTERNAL, MIHG_ENOMEM, MIHG_ECUDA, MIHG_ENCCL, MIHG_EFORMAT, MIHG_EIO = range(8)
 
 u64p = C.POINTER(C.c_uint64)
 u32p = C.POINTER(C.c_uint32)
@@ -80,6 +80,8 @@ SYMBOLS = [
     ("mihg_index_get_info", C.c_int, [C.c_void_p, C.POINTER(IndexInfo)]),
     ("mihg_table_get_info", C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(TableInfo)]),
     ("mihg_bucket_lookup", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, u32p, C.c_uint64, u64p]),
+    ("mihg_index_write", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("mihg_index_read", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
     ("mihg_index_codes", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("mihg_knn_batch", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint32, u32p, u32p,
                                  C.POINTER(Trace)]),
@@ -140,4 +142,13 @@ def check(rc: int) -> None:
         raise ValueError(msg)  # the reference throws std::invalid_argument
     if rc == MIHG_ENOMEM:
         raise MemoryError(msg)  # std::bad_alloc
+    if rc == MIHG_EFORMAT:
+        import re
+
+        from .io import FormatError
+
+        m = re.search(r"\(byte offset (\d+)\)$", msg)
+        raise FormatError(msg[: m.start()].rstrip() if m else msg, int(m.group(1)) if m else 0)
+    if rc == MIHG_EIO:
+        raise OSError(msg)
     raise MihgError(rc, msg)

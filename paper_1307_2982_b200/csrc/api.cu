@@ -7,6 +7,7 @@
 
 #include "../../include/mihg.h"
 #include "knn.cuh"
+#include "persist.cuh"
 
 struct mihg_index {
   mihg::Index* impl;
@@ -21,6 +22,9 @@ int guarded(F&& f) {
   try {
     f();
     return MIHG_OK;
+  } catch (const mihg::FormatError& e) {
+    g_err = e.what();
+    return MIHG_EFORMAT;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return MIHG_EINVAL;
@@ -34,6 +38,9 @@ int guarded(F&& f) {
     return MIHG_ECUDA;
   } catch (const std::exception& e) {
     g_err = e.what();
+    const std::string m = e.what();
+    if (m.rfind("cannot open", 0) == 0 || m.rfind("read failed", 0) == 0 || m.rfind("write failed", 0) == 0)
+      return MIHG_EIO;
     return MIHG_EINTERNAL;
   } catch (...) {
     g_err = "unknown error";
@@ -217,6 +224,26 @@ int mihg_bucket_lookup(const mihg_index* idx, uint32_t j, uint64_t value, uint32
       MIHG_CUDA(cudaMemcpy(out_ids, t.ids.get() + lo, w * 4, cudaMemcpyDeviceToHost));
       for (uint64_t i = 0; i < w; ++i) out_ids[i] += ix.id_base;
     }
+  });
+}
+
+int mihg_index_write(mihg_index* idx, const char* path) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    if (!path) throw mihg::InvalidArgument("null path");
+    if (ix.id_base) throw mihg::InvalidArgument("write_index: shard indexes (id_base != 0) are not files");
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    mihg::write_index(ix, path);
+  });
+}
+
+int mihg_index_read(const char* path, int device, mihg_index** out) {
+  return guarded([&] {
+    if (!path || !out) throw mihg::InvalidArgument("null argument");
+    DeviceGuard g(device);
+    mihg::BuildOptions opt;
+    *out = new mihg_index{mihg::read_index(path, device, opt)};
   });
 }
 

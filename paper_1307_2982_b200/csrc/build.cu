@@ -255,7 +255,10 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
 
   DeviceBuffer<uint32_t> keys(std::max<uint64_t>(n, 1), st);
   t->ids = DeviceBuffer<uint32_t>(std::max<uint64_t>(n, 1), st);
-  if (n) {
+  if (n && opt.pre) {  // tables from an index file: already in (key, id) order
+    MIHG_CUDA(cudaMemcpyAsync(keys.get(), (*opt.pre)[j].keys.data(), n * 4, cudaMemcpyHostToDevice, st));
+    MIHG_CUDA(cudaMemcpyAsync(t->ids.get(), (*opt.pre)[j].ids.data(), n * 4, cudaMemcpyHostToDevice, st));
+  } else if (n) {
     extract_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx.codes.get(), idx.W, n, idx.subs[j],
                                                           idx.d_positions.get(), keys.get(),
                                                           t->ids.get());

@@ -176,8 +176,12 @@ struct Diff<0> {
   }
 };
 
-constexpr uint32_t kInlineMax = 64;   // buckets up to this size are verified by the probing thread
-constexpr uint32_t kPieceSize = 256;  // bigger buckets are cut into warp-sized pieces
+// Buckets up to inline_max entries are verified by the probing warp; bigger ones are cut into
+// pieces of piece_size entries for the warp-per-piece kernel (MIHG_INLINE_MAX / MIHG_PIECE_SIZE).
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? uint32_t(std::atoi(e)) : dflt;
+}
 
 struct ProbeArgs {
   const uint64_t* codes;
@@ -205,6 +209,7 @@ struct ProbeArgs {
   Piece* pieces;            // nullable: no piece queue
   uint32_t* piece_count;
   uint32_t piece_cap;
+  uint32_t inline_max, piece_size;
   const uint64_t* binom;    // device_binomials()
   // L2-sliced rounds (slice_bits > 0): active queries grouped by the top t bits G of their
   // substring; units enumerated per (slice P, group G) pair, P-major, claimed in order.
@@ -462,12 +467,12 @@ __global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kerne
 #pragma unroll
       for (int b = 0; b < kLaneProbes; ++b) {
         n_cand += cnt[b];
-        if (cnt[b] > kInlineMax && p.pieces) {
-          const uint32_t np = (cnt[b] + kPieceSize - 1) / kPieceSize;
+        if (cnt[b] > p.inline_max && p.pieces) {
+          const uint32_t np = (cnt[b] + p.piece_size - 1) / p.piece_size;
           const uint32_t at = atomicAdd(p.piece_count, np);
           if (at + np <= p.piece_cap) {
             for (uint32_t t = 0; t < np; ++t)
-              p.pieces[at + t] = Piece{q, lo[b] + t * kPieceSize, min(kPieceSize, cnt[b] - t * kPieceSize), 0};
+              p.pieces[at + t] = Piece{q, lo[b] + t * p.piece_size, min(p.piece_size, cnt[b] - t * p.piece_size), 0};
             cnt[b] = 0;
           } else {
             for (uint32_t t = at; t < p.piece_cap && t < at + np; ++t) p.pieces[t] = Piece{q, 0, 0, 0};
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(kProbeThreads) mih_piece_kernel(ProbeArgs p) {
     uint64_t n_new = 0;
     for (uint32_t t0 = 0; t0 < pc.cnt; t0 += 64)
       verify_entries<W, kTrace>(p, ctx, t0 + lane < pc.cnt, pc.lo + t0 + lane, t0 + 32 + lane < pc.cnt,
-                        pc.lo + t0 + 32 + lane, qc, nw, n_new);
+                                pc.lo + t0 + 32 + lane, qc, nw, n_new);
     if (kTrace) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) n_new += __shfl_xor_sync(~0u, n_new, o);
@@ -892,6 +897,10 @@ ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   p.piece_count = ws.piece_count.get();
   p.piece_cap = kPieceQueue;
   p.binom = device_binomials();
+  static const uint32_t inline_max = env_u32("MIHG_INLINE_MAX", 64);
+  static const uint32_t piece_size = env_u32("MIHG_PIECE_SIZE", 256);
+  p.inline_max = inline_max;
+  p.piece_size = std::max<uint32_t>(32, piece_size);
   return p;
 }
 

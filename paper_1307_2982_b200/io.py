@@ -26,6 +26,35 @@ class FormatError(RuntimeError):  # io.hpp:35-44
         self.offset = offset
 
 
+def write_index(idx, path: str) -> None:
+    """write_index (io.hpp:335-358): the BMIX file, byte-identical to the reference's."""
+    _lib.check(_lib.lib().mihg_index_write(idx._h, path.encode()))
+
+
+def read_index(path: str, device: int = 0):
+    """read_index (io.hpp:360-425): validated load of a BMIX file (FormatError with byte offset);
+    the file's tables are loaded onto the GPU as given."""
+    import ctypes as C
+
+    from .codes import Partition
+    from .index import MihIndex
+
+    h = C.c_void_p()
+    _lib.check(_lib.lib().mihg_index_read(path.encode(), device, C.byref(h)))
+    # host-side mirror of the codes and partition (db(), partition() accessors)
+    with open(path, "rb") as f:
+        f.seek(8)
+        bits, n = struct.unpack("<IQ", f.read(12))
+        wpc = words_per_code(bits)
+        words = np.frombuffer(f.read(n * wpc * 8), dtype="<u8").astype(np.uint64).reshape(n, wpc)
+        (m,) = struct.unpack("<I", f.read(4))
+        subs = []
+        for _ in range(m):
+            (ln,) = struct.unpack("<I", f.read(4))
+            subs.append(list(np.frombuffer(f.read(4 * ln), dtype="<u4")))
+    return MihIndex(h, CodeDatabase(bits, words), Partition(bits, subs), bits, n, device, 0)
+
+
 def gen_uniform(n: int, bits: int, seed: int) -> CodeDatabase:
     if bits == 0 or bits > kMaxCodeBits:
         raise ValueError("gen_uniform: bad width")

@@ -185,6 +185,40 @@ def main():
         stats[name + "_spec"] = np.array([n, bits, seed, m], np.uint64)
     files["table_stats"] = stats
 
+    # BMIX index files written by the reference's write_index (io.hpp:335-358), io_test.cpp:141-176
+    # style shapes, plus its knn (k=5) and range (r = bits/4) answers on 10 queries each.
+    import tempfile
+    rng = np.random.default_rng(2)
+    bm = {}
+    case = 0
+    while case < 5:
+        bits = int(16 + rng.integers(0, 100))
+        m = int(2 + rng.integers(0, 6))
+        if (bits + m - 1) // m > 32:
+            continue
+        n = int(300 + rng.integers(0, 500))
+        codes = R.gen_uniform(n, bits, int(rng.integers(1, 1 << 40)))
+        qs = R.gen_uniform(10, bits, int(rng.integers(1, 1 << 40)))
+        h = R.build(codes, bits, m)
+        with tempfile.TemporaryDirectory() as td:
+            fp = os.path.join(td, "idx.bin")
+            assert R.lib.ref_write_index(h.h, fp.encode()) == 0
+            blob = np.frombuffer(open(fp, "rb").read(), np.uint8).copy()
+        ids, dists, tr = h.knn(qs, 5)
+        rr = bits // 4
+        roffs, rids, rd, rtr = [0], [], [], []
+        for qi in range(10):
+            a, b, t = h.range(qs[qi], rr)
+            rids.append(a); rd.append(b); rtr.append(t); roffs.append(roffs[-1] + a.size)
+        p_ = f"c{case}_"
+        bm.update({p_ + "bmix": blob, p_ + "spec": np.array([bits, m, n], np.uint64), p_ + "queries": qs,
+                   p_ + "knn_ids": ids, p_ + "knn_dists": dists, p_ + "knn_trace": tr,
+                   p_ + "range_r": np.array([rr], np.uint64), p_ + "range_offs": np.array(roffs, np.uint64),
+                   p_ + "range_ids": np.concatenate(rids).astype(np.uint32),
+                   p_ + "range_dists": np.concatenate(rd).astype(np.uint32), p_ + "range_trace": np.stack(rtr)})
+        case += 1
+    files["bmix_files"] = bm
+
     # gen_uniform pins (io.hpp:266-277): several widths and seeds.
     pins = {}
     for n, bits, seed in ((5, 64, 1), (7, 70, 181), (3, 256, 42), (4, 24, 501), (2, 130, 9)):

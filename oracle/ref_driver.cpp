@@ -124,6 +124,14 @@ int ref_gen_lsh(uint64_t fit_n, uint64_t enc_n, uint32_t dim, uint32_t group, do
   });
 }
 
+// gen_duplicated_bits (io.hpp:281-297), pins the CLI's `gen --mode correlated`.
+int ref_gen_duplicated(uint64_t n, uint32_t bits, uint32_t block, uint64_t seed, uint64_t* out) {
+  return guarded([&] {
+    mih::CodeDatabase db = mih::gen_duplicated_bits(n, bits, block, seed);
+    if (n) std::memcpy(out, db.raw_words().data(), db.raw_words().size() * sizeof(uint64_t));
+  });
+}
+
 int ref_index_build(const uint64_t* codes, uint64_t n, uint32_t bits, uint32_t m,
                     const uint32_t* lengths, const uint32_t* positions, void** out) {
   return guarded([&] {

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmihg.so")
+LIB_PATH = os.environ.get("MIHG_LIB_PATH") or os.path.join(_HERE, "libmihg.so")  # override: A/B builds
 
 MIHG_OK, MIHG_EINVAL, MIHG_EINTERNAL, MIHG_ENOMEM, MIHG_ECUDA, MIHG_ENCCL, MIHG_EFORMAT, MIHG_EIO = range(8)
 

@@ -390,7 +390,7 @@ constexpr int kProbeWarps = kProbeThreads / 32;
 // [off, off + cnt) holds t: 7-step binary search in shared memory), so bucket-size skew never
 // idles the warp. Buckets above kInlineMax go to the piece queue.
 template <int W, bool kTrace, int kLaneProbes>
-__global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kernel(ProbeArgs p) {
+__global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kernel(ProbeArgs p) {
   constexpr int kWarpBuckets = 32 * kLaneProbes;
   constexpr int kSearchSteps = kLaneProbes == 1 ? 5 : kLaneProbes == 2 ? 6 : 7;
   __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kProbeThreads, W == 1 ? 5 : 1) mih_probe_kerne
 
 // One warp per queued piece of a big bucket (64 entries per pass).
 template <int W, bool kTrace>
-__global__ void __launch_bounds__(kProbeThreads) mih_piece_kernel(ProbeArgs p) {
+__global__ void __launch_bounds__(kProbeThreads, 8) mih_piece_kernel(ProbeArgs p) {
   const uint32_t nw = W ? W : p.nw;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t npieces = min(*p.piece_count, p.piece_cap);

@@ -89,7 +89,7 @@ __device__ __noinline__ uint32_t compact_list(uint64_t* list, uint32_t& cnt, uin
 }
 
 template <int W, int QT>
-__global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(ScanArgs a) {
+__global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanArgs a) {
   extern __shared__ uint32_t s_hist[];  // kScanWarps * (bits + 1)
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nw = W ? W : a.nw;

@@ -211,6 +211,26 @@ int mihg_profile_read(mihg_profile* out);
 int mihg_gen_mixture_device(uint64_t first, uint64_t n, uint32_t bits, uint32_t dim, uint32_t comps,
                             uint64_t model_seed, uint64_t data_seed, uint64_t* d_out, void* stream);
 
+/* ---- substring optimisation ---- */
+
+/* estimate_correlations (optimize.hpp:47-92; replaces mih::estimate_correlations): |Pearson|
+ * between every pair of bit positions over n >= 2 codes (n * ceil(bits/64) words, host memory,
+ * or device memory on `device` when codes_on_device). The AND-popcount Gram matrix runs on the
+ * GPU; out_corr receives bits*bits doubles row-major (diagonal 1; 0 against constant bits),
+ * out_constant bits flags (CorrelationMatrix::is_constant), out_counts (nullable) the exact
+ * integer counts #(bit_i AND bit_j) (diagonal = ones). n < 2 -> MIHG_EINVAL (the reference's
+ * std::invalid_argument). Values are bitwise the reference's as built by its CMake on an FMA host. */
+int mihg_estimate_correlations(const uint64_t* codes, uint64_t n, uint32_t bits, int device,
+                               int codes_on_device, double* out_corr, uint8_t* out_constant,
+                               uint64_t* out_counts);
+
+/* greedy_assign (optimize.hpp:101-172; replaces mih::greedy_assign): host-only (no GPU needed).
+ * corr/constant as produced above; writes out_lengths[m] and the m sorted position lists
+ * concatenated into out_positions[bits] (the Partition's substrings). m == 0 or m > bits ->
+ * MIHG_EINVAL. Same std::mt19937_64 + std::uniform_int_distribution draw as the reference. */
+int mihg_greedy_assign(const double* corr, const uint8_t* constant, uint32_t bits, uint32_t m,
+                       uint64_t seed, uint32_t* out_lengths, uint32_t* out_positions);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,8 @@
 //   auto idx = mihg::MihIndex<>::build(db, partition);            // index.hpp:101-121
 //   auto res = idx.knn_search(q, k, &trace, &scratch);             // index.hpp:185-253
 //   idx.db(); idx.partition(); idx.num_tables();                    // index.hpp:143-146
+//   auto c = mihg::estimate_correlations<mih::CorrelationMatrix>(db); // optimize.hpp:47-92
+//   auto p = mihg::greedy_assign<mih::Partition>(c, m, seed);         // optimize.hpp:101-172
 //
 // It is duck-typed over the reference's own types, so a caller holding mih::CodeDatabase,
 // mih::Partition, mih::BinaryCode, mih::SearchTrace and mih::Neighbors switches by replacing
@@ -145,5 +147,42 @@ class MihIndex {
   uint32_t bits_ = 0, m_ = 0;
   uint64_t n_ = 0;
 };
+
+// estimate_correlations(sample) — optimize.hpp:47-92, Gram kernel on the GPU. CorrT: any type
+// constructible from the width with set(i, j, v) / set_constant(i) (mih::CorrelationMatrix).
+template <class CorrT, class DB>
+CorrT estimate_correlations(const DB& sample, int device = 0) {
+  const uint32_t b = sample.bits();
+  std::vector<double> corr(uint64_t{b} * b);
+  std::vector<uint8_t> constant(b);
+  check(mihg_estimate_correlations(sample.raw_words().data(), sample.size(), b, device, 0, corr.data(),
+                                   constant.data(), nullptr));
+  CorrT out(b);
+  for (uint32_t i = 0; i < b; ++i) {
+    if (constant[i]) out.set_constant(i);
+    for (uint32_t j = i + 1; j < b; ++j) out.set(i, j, corr[uint64_t{i} * b + j]);
+  }
+  return out;
+}
+
+// greedy_assign(corr, m, seed) — optimize.hpp:101-172 (host). PartT: constructible from
+// (bits, std::vector<std::vector<uint32_t>>) (mih::Partition); CorrT: bits(), at(), is_constant().
+template <class PartT, class CorrT>
+PartT greedy_assign(const CorrT& corr, uint32_t m, uint64_t seed) {
+  const uint32_t b = corr.bits();
+  std::vector<double> v(uint64_t{b} * b);
+  std::vector<uint8_t> constant(b);
+  for (uint32_t i = 0; i < b; ++i) {
+    constant[i] = corr.is_constant(i) ? 1 : 0;
+    for (uint32_t j = 0; j < b; ++j) v[uint64_t{i} * b + j] = corr.at(i, j);
+  }
+  std::vector<uint32_t> lengths(m), positions(b);
+  check(mihg_greedy_assign(v.data(), constant.data(), b, m, seed, lengths.data(), positions.data()));
+  std::vector<std::vector<uint32_t>> subs(m);
+  uint32_t at = 0;
+  for (uint32_t j = 0; j < m; ++j)
+    for (uint32_t t = 0; t < lengths[j]; ++t) subs[j].push_back(positions[at++]);
+  return PartT(b, std::move(subs));
+}
 
 }  // namespace mihg

@@ -69,6 +69,39 @@ class _Lib:
         if rc:
             raise OracleError(self._err().decode())
 
+    def estimate_correlations(self, codes, bits):
+        """optimize.hpp:47-92 -> (corr[b,b] f64, constant[b] bool, counts[b,b] u64 or None)."""
+        codes = np.ascontiguousarray(codes, np.uint64).reshape(-1)
+        n = codes.size // wpc(bits)
+        corr = np.zeros((bits, bits), np.float64)
+        const = np.zeros(bits, np.uint8)
+        dp, cp = corr.ctypes.data_as(C.POINTER(C.c_double)), const.ctypes.data_as(C.POINTER(C.c_uint8))
+        if self.prefix == "or_":
+            counts = np.zeros((bits, bits), np.uint64)
+            self._check(self.lib.or_estimate_correlations(_p64(codes), C.c_uint64(n), C.c_uint32(bits),
+                                                          dp, cp, _p64(counts)))
+        else:
+            counts = None
+            self._check(self.lib.ref_estimate_correlations(_p64(codes), C.c_uint64(n), C.c_uint32(bits),
+                                                           dp, cp))
+        return corr, const.astype(bool), counts
+
+    def greedy_assign(self, corr, constant, m, seed):
+        """optimize.hpp:101-172 -> list of m sorted position lists."""
+        corr = np.ascontiguousarray(corr, np.float64)
+        const = np.ascontiguousarray(constant, np.uint8)
+        bits = corr.shape[0]
+        lengths = np.zeros(max(m, 1), np.uint32)
+        pos = np.zeros(bits, np.uint32)
+        self._check(getattr(self.lib, self.prefix + "greedy_assign")(
+            corr.ctypes.data_as(C.POINTER(C.c_double)), const.ctypes.data_as(C.POINTER(C.c_uint8)),
+            C.c_uint32(bits), C.c_uint32(m), C.c_uint64(seed), _p32(lengths), _p32(pos)))
+        out, at = [], 0
+        for L in lengths[:m]:
+            out.append([int(x) for x in pos[at:at + L]])
+            at += int(L)
+        return out
+
 
 class Port(_Lib):
     """The C restatement (mih_oracle.c)."""

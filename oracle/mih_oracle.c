@@ -600,3 +600,163 @@ int or_gen_mixture(uint64_t first, uint64_t n, uint32_t bits, uint32_t dim, uint
   free(mu);
   return 0;
 }
+
+/* ---- substring optimisation (optimize.hpp) ---- */
+
+/* estimate_correlations (optimize.hpp:47-92): bit columns as packed bitsets, ones(i) and
+ * ones(i AND j) by popcount, |Pearson| = |p_ij - p_i p_j| / sqrt(var_i var_j) clamped to 1;
+ * bits with zero sample variance are flagged constant and stay 0 against every other bit.
+ * `counts` (optional, b*b) receives the integer AND counts (diagonal = ones).
+ * The reference as its CMake compiles it (-O3 -march=native; g++ contracts by default on an FMA
+ * host) evaluates p_ij - p_i*p_j as fma(-p_i, p_j, p_ij): restated explicitly, pinned bitwise. */
+int or_estimate_correlations(const uint64_t* codes, uint64_t n, uint32_t bits, double* corr,
+                             uint8_t* constant, uint64_t* counts) {
+  if (n < 2) return fail(1, "estimate_correlations: need at least 2 codes");
+  const uint32_t wpc = wpc_of(bits);
+  const uint64_t cw = (n + 63) / 64;
+  uint64_t* cols = (uint64_t*)calloc((size_t)bits * cw, 8);
+  uint64_t* ones = (uint64_t*)malloc((size_t)bits * 8);
+  double* var = (double*)malloc((size_t)bits * sizeof(double));
+  if (!cols || !ones || !var) {
+    free(cols);
+    free(ones);
+    free(var);
+    return fail(3, "bad_alloc");
+  }
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t pos = 0; pos < bits; ++pos)
+      if ((codes[i * wpc + pos / 64] >> (pos % 64)) & 1) cols[(uint64_t)pos * cw + (i >> 6)] |= 1ULL << (i & 63);
+  for (uint32_t i = 0; i < bits; ++i) {
+    uint64_t c = 0;
+    for (uint64_t w = 0; w < cw; ++w) c += (uint64_t)__builtin_popcountll(cols[(uint64_t)i * cw + w]);
+    ones[i] = c;
+    const double p = (double)c / (double)n;
+    var[i] = p * (1.0 - p);
+    constant[i] = (c == 0 || c == n) ? 1 : 0;
+  }
+  for (uint32_t i = 0; i < bits; ++i)
+    for (uint32_t j = 0; j < bits; ++j) corr[(uint64_t)i * bits + j] = i == j ? 1.0 : 0.0;
+  for (uint32_t i = 0; i < bits; ++i) {
+    if (counts) counts[(uint64_t)i * bits + i] = ones[i];
+    for (uint32_t j = i + 1; j < bits; ++j) {
+      uint64_t c = 0;
+      for (uint64_t w = 0; w < cw; ++w)
+        c += (uint64_t)__builtin_popcountll(cols[(uint64_t)i * cw + w] & cols[(uint64_t)j * cw + w]);
+      if (counts) counts[(uint64_t)i * bits + j] = counts[(uint64_t)j * bits + i] = c;
+      if (var[i] == 0.0 || var[j] == 0.0) continue;
+      const double pi = (double)ones[i] / (double)n, pj = (double)ones[j] / (double)n;
+      const double pij = (double)c / (double)n;
+      double v = __builtin_fabs(__builtin_fma(-pi, pj, pij)) / __builtin_sqrt(var[i] * var[j]);
+      if (v > 1.0) v = 1.0;
+      corr[(uint64_t)i * bits + j] = corr[(uint64_t)j * bits + i] = v;
+    }
+  }
+  free(cols);
+  free(ones);
+  free(var);
+  return 0;
+}
+
+/* std::uniform_int_distribution<size_t>(0, range-1) over mt19937_64 as libstdc++ draws it:
+ * the generator's range is exactly 2^64, so it downscales with Lemire's multiply-shift and
+ * rejects low products below (2^64 - range) mod range. */
+static uint64_t uniform_below(mt64* g, uint64_t range) {
+  unsigned __int128 prod = (unsigned __int128)mt64_next(g) * range;
+  uint64_t low = (uint64_t)prod;
+  if (low < range) {
+    const uint64_t threshold = (0 - range) % range;
+    while (low < threshold) {
+      prod = (unsigned __int128)mt64_next(g) * range;
+      low = (uint64_t)prod;
+    }
+  }
+  return (uint64_t)(prod >> 64);
+}
+
+static void take_value(uint32_t* v, uint32_t* len, uint32_t value) {
+  uint32_t i = 0;
+  while (v[i] != value) ++i;
+  memmove(v + i, v + i + 1, (size_t)(*len - i - 1) * 4);
+  --*len;
+}
+
+/* greedy_assign (optimize.hpp:101-172): chain initialisation from a seed-chosen opener, then
+ * rounds giving each substring with spare capacity the unused bit of least worst-case
+ * correlation with its current bits (ties to the lowest index), constant bits last
+ * round-robin; each substring's positions sorted ascending. */
+int or_greedy_assign(const double* corr, const uint8_t* constant, uint32_t bits, uint32_t m,
+                     uint64_t seed, uint32_t* lengths, uint32_t* positions) {
+  if (m == 0 || m > bits) return fail(1, "greedy_assign: need 1 <= m <= bits");
+  uint32_t *cap = calloc(m, 4), *len = calloc(m, 4), *sub = calloc((size_t)m * bits, 4);
+  uint32_t *pool = malloc((size_t)bits * 4), *consts = malloc((size_t)bits * 4);
+  mt64* g = malloc(sizeof(mt64));
+  if (!cap || !len || !sub || !pool || !consts || !g) {
+    free(cap); free(len); free(sub); free(pool); free(consts); free(g);
+    return fail(3, "bad_alloc");
+  }
+  uint32_t np = 0, nc = 0;
+  for (uint32_t j = 0; j < m; ++j) cap[j] = bits / m + (j < bits % m ? 1 : 0);
+  for (uint32_t i = 0; i < bits; ++i) {
+    if (constant[i]) consts[nc++] = i;
+    else pool[np++] = i;
+  }
+#define SUB(j, t) sub[(size_t)(j) * bits + (t)]
+  if (np) {
+    mt64_seed(g, seed);
+    const uint32_t first = pool[uniform_below(g, np)];
+    SUB(0, len[0]++) = first;
+    take_value(pool, &np, first);
+    for (uint32_t j = 1; j < m && np; ++j) {
+      const uint32_t prev = len[j - 1] == 0 ? first : SUB(j - 1, 0);
+      uint32_t best = pool[0];
+      double best_c = -1.0;
+      for (uint32_t t = 0; t < np; ++t) {
+        const double c = corr[(uint64_t)pool[t] * bits + prev];
+        if (c > best_c) {
+          best_c = c;
+          best = pool[t];
+        }
+      }
+      SUB(j, len[j]++) = best;
+      take_value(pool, &np, best);
+    }
+  }
+  while (np) {
+    int any = 0;
+    for (uint32_t j = 0; j < m && np; ++j) {
+      if (len[j] >= cap[j]) continue;
+      any = 1;
+      uint32_t best = pool[0];
+      double best_worst = 2.0;
+      for (uint32_t t = 0; t < np; ++t) {
+        double worst = 0.0;
+        for (uint32_t o = 0; o < len[j]; ++o) {
+          const double c = corr[(uint64_t)pool[t] * bits + SUB(j, o)];
+          if (c > worst) worst = c;
+        }
+        if (worst < best_worst) {
+          best_worst = worst;
+          best = pool[t];
+        }
+      }
+      SUB(j, len[j]++) = best;
+      take_value(pool, &np, best);
+    }
+    if (!any) break;
+  }
+  uint32_t j = 0;
+  for (uint32_t t = 0; t < nc; ++t) {
+    while (len[j] >= cap[j]) j = (j + 1) % m;
+    SUB(j, len[j]++) = consts[t];
+    j = (j + 1) % m;
+  }
+  uint32_t at = 0;
+  for (uint32_t q = 0; q < m; ++q) {
+    qsort(&SUB(q, 0), len[q], 4, u32_cmp);
+    lengths[q] = len[q];
+    for (uint32_t t = 0; t < len[q]; ++t) positions[at++] = SUB(q, t);
+  }
+#undef SUB
+  free(cap); free(len); free(sub); free(pool); free(consts); free(g);
+  return 0;
+}

@@ -30,6 +30,11 @@ int or_scan_knn(const uint64_t* codes, uint64_t n, uint32_t bits, const uint64_t
 int or_gen_mixture(uint64_t first, uint64_t n, uint32_t bits, uint32_t dim, uint32_t comps,
                    uint64_t model_seed, uint64_t data_seed, uint64_t* out, int nthreads);
 
+int or_estimate_correlations(const uint64_t* codes, uint64_t n, uint32_t bits, double* corr,
+                             uint8_t* constant, uint64_t* counts);
+int or_greedy_assign(const double* corr, const uint8_t* constant, uint32_t bits, uint32_t m,
+                     uint64_t seed, uint32_t* lengths, uint32_t* positions);
+
 #ifdef __cplusplus
 }
 #endif

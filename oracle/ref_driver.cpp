@@ -7,6 +7,7 @@
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline / --impl reference legs
 // load it, as the checker or the timed CPU baseline.
 //
+// optimize.hpp (estimate_correlations / greedy_assign) needs only codes.hpp and is included.
 // mih.hpp / costmodel.hpp are deliberately NOT included: they pull in <gmpxx.h>, which is
 // absent. Every entry point catches C++ exceptions and maps them to
 // integer codes (1 = std::invalid_argument, 2 = FormatError/other, 3 = bad_alloc).
@@ -22,6 +23,7 @@
 #include "mih/codes.hpp"
 #include "mih/index.hpp"
 #include "mih/io.hpp"
+#include "mih/optimize.hpp"
 #include "mih/scan.hpp"
 #include "mih/table.hpp"
 
@@ -286,6 +288,36 @@ int ref_write_index(void* h, const char* path) {
 
 int ref_read_index(const char* path, void** out) {
   return guarded([&] { *out = new mih::MihIndex(mih::read_index(path)); });
+}
+
+// estimate_correlations (optimize.hpp:47-92): b*b |Pearson| matrix (row-major) + constant flags.
+int ref_estimate_correlations(const uint64_t* codes, uint64_t n, uint32_t bits, double* corr,
+                              uint8_t* constant) {
+  return guarded([&] {
+    const mih::CorrelationMatrix c = mih::estimate_correlations(make_db(codes, n, bits));
+    for (uint32_t i = 0; i < bits; ++i) {
+      constant[i] = c.is_constant(i) ? 1 : 0;
+      for (uint32_t j = 0; j < bits; ++j) corr[uint64_t{i} * bits + j] = c.at(i, j);
+    }
+  });
+}
+
+// greedy_assign (optimize.hpp:101-172) over a given matrix; lengths[m] + concatenated positions.
+int ref_greedy_assign(const double* corr, const uint8_t* constant, uint32_t bits, uint32_t m,
+                      uint64_t seed, uint32_t* lengths, uint32_t* positions) {
+  return guarded([&] {
+    mih::CorrelationMatrix c(bits);
+    for (uint32_t i = 0; i < bits; ++i) {
+      if (constant[i]) c.set_constant(i);
+      for (uint32_t j = i + 1; j < bits; ++j) c.set(i, j, corr[uint64_t{i} * bits + j]);
+    }
+    const mih::Partition p = mih::greedy_assign(c, m, seed);
+    uint32_t at = 0;
+    for (uint32_t j = 0; j < p.m(); ++j) {
+      lengths[j] = p.length(j);
+      for (uint32_t pos : p.positions(j)) positions[at++] = pos;
+    }
+  });
 }
 
 }  // extern "C"

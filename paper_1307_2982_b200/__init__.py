@@ -9,10 +9,12 @@ from .codes import (BinaryCode, CodeDatabase, Partition, consecutive_partition, 
 from .index import (MihIndex, Neighbor, SearchTrace, TableStats, build_index, neighbor_less,
                     scan_knn)
 from .io import FormatError, gen_uniform, read_codes, read_index, write_codes, write_index
+from .optimize import CorrelationMatrix, estimate_correlations, greedy_assign
 
 __all__ = [
     "BinaryCode", "CodeDatabase", "Partition", "consecutive_partition", "extract_substring",
     "hamming_distance", "kMaxCodeBits", "words_per_code", "MihIndex", "Neighbor", "SearchTrace",
     "TableStats", "build_index", "neighbor_less", "scan_knn", "FormatError", "gen_uniform",
-    "read_codes", "write_codes", "read_index", "write_index",
+    "read_codes", "write_codes", "read_index", "write_index", "CorrelationMatrix",
+    "estimate_correlations", "greedy_assign",
 ]

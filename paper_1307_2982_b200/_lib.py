@@ -109,6 +109,10 @@ SYMBOLS = [
     ("mihg_gen_mixture_device", C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                                           C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p,
                                           C.c_void_p]),
+    ("mihg_estimate_correlations", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_int,
+                                             C.POINTER(C.c_double), C.POINTER(C.c_uint8), u64p]),
+    ("mihg_greedy_assign", C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.c_uint32,
+                                     C.c_uint32, C.c_uint64, u32p, u32p]),
     ("mihg_profile_enable", C.c_int, [C.c_int]),
     ("mihg_profile_reset", None, []),
     ("mihg_profile_read", C.c_int, [C.POINTER(Profile)]),

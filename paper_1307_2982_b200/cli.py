@@ -1,12 +1,13 @@
 """Command-line front end on the GPU index — the hot-path subcommands of the reference CLI
-(/root/reference/proj/tools/mih.cpp): gen / build / query / benchmark, same options, report
-schemas and exit codes (0 ok, 1 usage, 2 data/format error, 3 benchmark verification mismatch,
-tools/mih.cpp:28-31). costmodel / optimize are out of scope.
+(/root/reference/proj/tools/mih.cpp): gen / build / query / benchmark / optimize, same options,
+report schemas and exit codes (0 ok, 1 usage, 2 data/format error, 3 benchmark verification
+mismatch, tools/mih.cpp:28-31). costmodel is out of scope.
 
     python -m paper_1307_2982_b200.cli gen --mode uniform --n 20000 --bits 64 --seed 11 --out data.bin
     python -m paper_1307_2982_b200.cli build --dataset data.bin --tables 4 --stats --out idx.bin
     python -m paper_1307_2982_b200.cli query --index idx.bin --queries q.bin --k 5 --out knn.csv
     python -m paper_1307_2982_b200.cli benchmark --dataset data.bin --queries q.bin --k 3 --radius 6
+    python -m paper_1307_2982_b200.cli optimize --dataset data.bin --tables 4 --seed 7 --out part.json
 """
 from __future__ import annotations
 
@@ -259,6 +260,23 @@ def run_benchmark(a) -> int:
     return EXIT_OK
 
 
+def run_optimize(a) -> int:
+    """tools/mih.cpp:502-512: estimate_correlations (GPU Gram kernel) + greedy_assign, written as
+    partition JSON {bits, substrings} (save_partition_json, :57-64) for build --partition."""
+    import paper_1307_2982_b200 as mg
+
+    db = mg.read_codes(a.dataset)
+    m = a.tables if a.tables > 0 else choose_num_tables(db.bits(), max(db.size(), 2))
+    p = mg.greedy_assign(mg.estimate_correlations(db, device=a.device), m, a.seed)
+    try:
+        with open(a.out, "w") as f:
+            f.write(json.dumps({"bits": p.bits(), "substrings": p.substrings()}, indent=2) + "\n")
+    except OSError as e:
+        raise DataError(f"cannot open for writing: {a.out}") from e
+    print(f"wrote {a.out} (m={m})")
+    return EXIT_OK
+
+
 class _Parser(argparse.ArgumentParser):
     def error(self, message):  # usage errors exit 1 (tools/mih.cpp:596-600)
         self.print_usage(sys.stderr)
@@ -305,6 +323,12 @@ def main(argv=None) -> int:
     be.add_argument("--out", default="")
     be.add_argument("--format", default="csv", choices=["csv", "json"])
     be.add_argument("--device", type=int, default=0)
+    o = sub.add_parser("optimize", help="fit a correlation-aware partition")
+    o.add_argument("--dataset", required=True)
+    o.add_argument("--tables", type=int, default=0)
+    o.add_argument("--seed", type=int, default=0)
+    o.add_argument("--out", required=True)
+    o.add_argument("--device", type=int, default=0)
     a = ap.parse_args(argv)
     if not a.cmd:
         ap.print_usage(sys.stderr)
@@ -312,7 +336,8 @@ def main(argv=None) -> int:
     import paper_1307_2982_b200 as mg
 
     try:
-        return {"gen": run_gen, "build": run_build, "query": run_query, "benchmark": run_benchmark}[a.cmd](a)
+        return {"gen": run_gen, "build": run_build, "query": run_query, "benchmark": run_benchmark,
+                "optimize": run_optimize}[a.cmd](a)
     except UsageError as e:
         print(f"usage error: {e}", file=sys.stderr)
         return EXIT_USAGE

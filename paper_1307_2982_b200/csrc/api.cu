@@ -7,6 +7,7 @@
 
 #include "../../include/mihg.h"
 #include "knn.cuh"
+#include "optimize.cuh"
 #include "persist.cuh"
 
 struct mihg_index {
@@ -437,6 +438,43 @@ int mihg_gen_uniform_range(uint64_t first, uint64_t n, uint32_t bits, uint64_t s
       for (uint32_t k = 0; k < wpc; ++k) w[k] = rng();
       w[wpc - 1] &= mask;
     }
+  });
+}
+
+int mihg_estimate_correlations(const uint64_t* codes, uint64_t n, uint32_t bits, int device,
+                               int codes_on_device, double* out_corr, uint8_t* out_constant,
+                               uint64_t* out_counts) {
+  return guarded([&] {
+    if (n < 2) throw mihg::InvalidArgument("estimate_correlations: need at least 2 codes");
+    if (bits == 0 || bits > mihg::kMaxCodeBits) throw mihg::InvalidArgument("estimate_correlations: bad width");
+    if (!codes || !out_corr || !out_constant) throw mihg::InvalidArgument("estimate_correlations: null pointer");
+    DeviceGuard g(device);
+    cudaStream_t st;
+    MIHG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<uint64_t> counts(uint64_t(bits) * bits);
+    try {
+      mihg::DeviceBuffer<uint64_t> d_counts(counts.size(), st);
+      MIHG_CUDA(cudaMemsetAsync(d_counts.get(), 0, counts.size() * 8, st));
+      mihg::and_count_gram(codes, n, bits, codes_on_device != 0, d_counts.get(), st);
+      MIHG_CUDA(cudaMemcpyAsync(counts.data(), d_counts.get(), counts.size() * 8, cudaMemcpyDeviceToHost, st));
+      MIHG_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamDestroy(st);
+    for (uint32_t i = 0; i < bits; ++i)  // the kernel fills the upper-triangle tiles only
+      for (uint32_t j = i + 1; j < bits; ++j) counts[uint64_t(j) * bits + i] = counts[uint64_t(i) * bits + j];
+    if (out_counts) std::memcpy(out_counts, counts.data(), counts.size() * 8);
+    mihg::finish_correlations(counts.data(), n, bits, out_corr, out_constant);
+  });
+}
+
+int mihg_greedy_assign(const double* corr, const uint8_t* constant, uint32_t bits, uint32_t m,
+                       uint64_t seed, uint32_t* out_lengths, uint32_t* out_positions) {
+  return guarded([&] {
+    if (!corr || !constant || !out_lengths || !out_positions) throw mihg::InvalidArgument("greedy_assign: null pointer");
+    mihg::greedy_assign(corr, constant, bits, m, seed, out_lengths, out_positions);
   });
 }
 

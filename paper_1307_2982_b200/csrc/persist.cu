@@ -197,15 +197,13 @@ Index* read_index(const std::string& path, int device, const BuildOptions& base_
         if (starts[i] > starts[i + 1]) throw invalid("table group starts not monotone");
       arena += uint64_t(c) + 1 + e;
       if (arena > (uint64_t(1) << 32)) throw invalid("table arena exceeds 2^32 slots");
-      uint32_t mm = mask, b = 0;
+      uint32_t mm = mask;
       t.keys.resize(at + e);
       for (uint32_t i = 0; i < c; ++i) {  // bucket i of the group = i-th set bit of the mask
         const uint32_t bit = uint32_t(__builtin_ctz(mm));
         mm &= mm - 1;
         for (uint32_t x = starts[i]; x < starts[i + 1]; ++x) t.keys[at + x] = uint32_t(gid * 32 + bit);
-        b = bit;
       }
-      (void)b;
       total += e;
       prev_g = gid;
       first = false;

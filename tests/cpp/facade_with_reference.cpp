@@ -11,6 +11,7 @@
 
 #include "mih/index.hpp"
 #include "mih/io.hpp"
+#include "mih/optimize.hpp"
 #include "mih/scan.hpp"
 #include "mihg/mih_gpu.hpp"
 
@@ -51,6 +52,29 @@ int main() {
   if (!gpu.knn_search(mih::BinaryCode{qw, 64}, 0).empty()) ++bad;
   try {
     mihg::MihIndex<mih::Neighbor>::build(db, mih::consecutive_partition(32, 2));
+    ++bad;
+  } catch (const std::invalid_argument&) {
+  }
+  // substring optimisation: the GPU Gram path vs the reference's estimate_correlations (bitwise)
+  // and greedy_assign over the reference's own matrix type (optimize.hpp)
+  for (uint32_t bits : {16u, 100u, 256u}) {
+    mih::CodeDatabase d = mih::gen_duplicated_bits(3000, bits, 4, 40 + bits);
+    const mih::CorrelationMatrix want = mih::estimate_correlations(d);
+    const auto got = mihg::estimate_correlations<mih::CorrelationMatrix>(d);
+    for (uint32_t i = 0; i < bits; ++i) {
+      if (want.is_constant(i) != got.is_constant(i)) ++bad;
+      for (uint32_t j = 0; j < bits; ++j)
+        if (want.at(i, j) != got.at(i, j)) ++bad;
+    }
+    for (uint32_t m : {2u, 4u}) {
+      if (!(mih::greedy_assign(want, m, 7 + m) == mihg::greedy_assign<mih::Partition>(got, m, 7 + m))) {
+        std::printf("greedy_assign mismatch bits=%u m=%u\n", bits, m);
+        ++bad;
+      }
+    }
+  }
+  try {
+    mihg::estimate_correlations<mih::CorrelationMatrix>(mih::CodeDatabase::zeros(3, 1));
     ++bad;
   } catch (const std::invalid_argument&) {
   }

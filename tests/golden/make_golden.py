@@ -40,9 +40,89 @@ def digest(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-def main():
+def optimize_codes(spec):
+    """Regenerate an optimize-case input from its spec (kind, n, bits, block, seed): 'dup' =
+    gen_duplicated_bits (io.hpp:281-297), 'uni' = gen_uniform (io.hpp:266-277). Both
+    regenerators are pinned against the reference elsewhere (test_cli / gen_uniform_pins)."""
+    from paper_1307_2982_b200 import gen_uniform
+    from paper_1307_2982_b200.cli import gen_duplicated_bits
+
+    kind, n, bits, block, seed = spec
+    if kind == "dup":
+        return gen_duplicated_bits(n, bits, block, seed).raw_words()
+    return gen_uniform(n, bits, seed).raw_words()
+
+
+# (name, spec or None for stored codes, [(m, seed), ...], store the full matrix?)
+OPTIMIZE_CASES = [
+    ("dup16", ("dup", 3000, 16, 2, 21), [(4, 0), (4, 1), (4, 77)], True),       # optimize_test.cpp:87-102
+    ("dup32", ("dup", 2000, 32, 4, 9), [(4, 123)], True),                      # :122-130
+    ("dup32_load", ("dup", 20000, 32, 4, 31), [(4, 7)], True),                 # :145-170
+    ("uni24", ("uni", 400, 24, 0, 3), [(1, 0), (3, 5), (24, 9)], True),        # :64-82
+    ("accept10", ("dup", 100000, 128, 4, 0xD00D0001), [(8, 0xD00D0003)], True),  # acceptance.cpp:462-490
+    ("dup100", ("dup", 777, 100, 4, 6), [(3, 1), (7, 2)], True),
+    ("dup256", ("dup", 5000, 256, 8, 7), [(8, 3), (16, 4)], False),
+    ("dup1000", ("dup", 3000, 1000, 8, 11), [(32, 5)], False),
+]
+
+
+def optimize_fixture(R):
+    """estimate_correlations + greedy_assign from the reference (optimize.hpp) on the cases of
+    optimize_test.cpp and acceptance criterion 10, plus multi-word widths for the GPU kernel."""
+    out = {}
+
+    def put(name, codes, bits, parts, full):
+        corr, const, _ = R.estimate_correlations(codes, bits)
+        out[name + "_const"] = const.astype(np.uint8)
+        if full:
+            out[name + "_corr"] = corr
+        out[name + "_corr_sha256"] = np.frombuffer(bytes.fromhex(digest(corr)), np.uint8)
+        for m, seed in parts:
+            subs = R.greedy_assign(corr, const, m, seed)
+            out[f"{name}_part_m{m}_s{seed}"] = np.array([x for sub in subs for x in sub], np.uint32)
+            out[f"{name}_lens_m{m}_s{seed}"] = np.array([len(sub) for sub in subs], np.uint32)
+
+    # hand-built inputs (optimize_test.cpp:16-62): codes stored verbatim
+    hand = np.array([[0b000], [0b011], [0b100], [0b111]], np.uint64)
+    anti = np.array([[0b01], [0b10], [0b01], [0b10]], np.uint64)
+    cbits = np.array([[0b001 | ((i % 2 == 0) << 1)] for i in range(5)], np.uint64)
+    rng = np.random.default_rng(14)  # HandlesConstantBits (:132-143): 4 random bits of 8
+    c8 = np.array([[int(rng.integers(0, 16))] for _ in range(100)], np.uint64)
+    for name, codes, bits, parts in (("hand", hand, 3, [(1, 0), (3, 0)]), ("anti", anti, 2, [(2, 0)]),
+                                     ("constbits", cbits, 3, [(2, 0), (3, 1)]), ("const8", c8, 8, [(4, 5)])):
+        out[name + "_codes"] = codes
+        out[name + "_bits"] = np.array([bits], np.uint32)
+        out[name + "_parts"] = np.array(parts, np.uint64)
+        put(name, codes, bits, parts, True)
+    for name, spec, parts, full in OPTIMIZE_CASES:
+        codes = optimize_codes(spec)
+        out[name + "_spec"] = np.array([0 if spec[0] == "dup" else 1] + list(spec[1:]), np.uint64)
+        out[name + "_parts"] = np.array(parts, np.uint64)
+        put(name, codes, spec[2], parts, full)
+    # ProducesValidBalancedPartitions (:104-120): random widths / table counts
+    rng = np.random.default_rng(8)
+    trials = []
+    for t in range(30):
+        bits = int(4 + rng.integers(0, 60))
+        m = int(1 + rng.integers(0, min(bits, 9)))
+        seed = int(rng.integers(0, 1 << 62))
+        trials.append((bits, m, seed))
+        codes = optimize_codes(("uni", 200, bits, 0, 1000 + t))
+        corr, const, _ = R.estimate_correlations(codes, bits)
+        subs = R.greedy_assign(corr, const, m, seed)
+        out[f"trial{t}_part"] = np.array([x for sub in subs for x in sub], np.uint32)
+        out[f"trial{t}_lens"] = np.array([len(sub) for sub in subs], np.uint32)
+    out["trials"] = np.array(trials, np.uint64)
+    return out
+
+
+def main(only=None):
     R = oracle.ref()
     files = {}
+    files["optimize"] = optimize_fixture(R)
+    if only == "optimize":
+        files = {"optimize": files["optimize"]}
+        return save(files)
 
     # index_test.cpp:73-94 HandWorkedKnn (and scan_test.cpp:14-19 tiny_db)
     codes = np.array([[0], [1], [63]], np.uint64)
@@ -225,6 +305,10 @@ def main():
         pins[f"gen_{n}_{bits}_{seed}"] = R.gen_uniform(n, bits, seed)
     files["gen_uniform_pins"] = pins
 
+    save(files)
+
+
+def save(files):
     for name, d in files.items():
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in d.items()})
@@ -232,4 +316,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

@@ -80,3 +80,19 @@ def test_cli_end_to_end(cuda_ok, tmp_path):
     assert all(need <= set(r) for r in rows)
     assert run(["query", "--index", "idx.bin", "--queries", "q.bin", "--k", "2", "--radius", "3"], tmp_path).returncode == 1
     assert run(["query", "--index", "idx.bin", "--queries", "q32.bin", "--k", "2"], tmp_path).returncode == 2
+
+
+@pytest.mark.gpu
+def test_cli_optimize_then_build(cuda_ok, tmp_path):
+    """optimize (tools/mih.cpp:502-512) writes a partition JSON that build --partition accepts; on
+    block-correlated codes it separates every duplicated block (optimize_test.cpp:87-102)."""
+    assert run(["gen", "--mode", "correlated", "--n", "3000", "--bits", "16", "--block", "2", "--seed", "21",
+                "--out", "dup.bin"], tmp_path).returncode == 0
+    r = run(["optimize", "--dataset", "dup.bin", "--tables", "4", "--seed", "77", "--out", "part.json"], tmp_path)
+    assert r.returncode == 0, r.stderr
+    j = json.load(open(tmp_path / "part.json"))
+    assert j["bits"] == 16 and len(j["substrings"]) == 4
+    assert all(len({x // 2 for x in s}) == len(s) == 4 for s in j["substrings"])
+    r = run(["build", "--dataset", "dup.bin", "--partition", "part.json", "--out", "idx.bin"], tmp_path)
+    assert r.returncode == 0, r.stderr
+    assert run(["optimize", "--dataset", "missing.bin", "--out", "p.json"], tmp_path).returncode == 2

@@ -451,7 +451,7 @@ def main():
     traffic = None
     tp = os.path.join(ROOT, "profiles", "r01", f"traffic_c{args.config}.json")
     if (os.path.exists(tp) and world == 1 and cfg["n"] == CONFIGS[args.config]["n"]
-            and cfg["nq"] == CONFIGS[args.config]["nq"]):
+            and cfg["nq"] == CONFIGS[args.config]["nq"] and cfg["k"] == CONFIGS[args.config]["k"]):
         tj = json.load(open(tp))
         traffic = {"dram_bytes_per_step": tj["dram_bytes_per_step"], "over_alg_bytes": tj["traffic_over_alg"],
                    "source": os.path.relpath(tp, ROOT)}
@@ -476,6 +476,8 @@ def main():
                     "alg_bytes_per_step": alg_bytes, "probe_ms_per_step": probe_ms,
                     "probe_launches_per_step": probe_launches,
                 "hybrid_scan_queries_per_step": (prof1.switched_queries - prof0.switched_queries) / args.steps,
+                    "rerun_queries_per_step": (prof1.rerun_queries - prof0.rerun_queries) / args.steps,
+                    "rerun_ms_per_step": (prof1.rerun_ms - prof0.rerun_ms) / args.steps,
                     "step_frac_of_roofline": (alg_bytes / (ms_per_step / 1000.0) / 1e9) / peak,
                     "popc64_per_step": popc64,
                     "mean_trace": {"lookups": float(lookups.mean()), "candidates": float(cands.mean()),

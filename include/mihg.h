@@ -199,6 +199,8 @@ typedef struct mihg_profile {
   double scan_ms;
   uint64_t scan_launches;
   uint64_t switched_queries; /* untraced kNN queries finished by the exhaustive scan (hybrid) */
+  uint64_t rerun_queries;    /* queries whose candidate buffer overflowed (exact re-run pass) */
+  double rerun_ms;           /* host wall time spent in re-run passes (synchronous) */
 } mihg_profile;
 int mihg_profile_enable(int on);
 void mihg_profile_reset(void);

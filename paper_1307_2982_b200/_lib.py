@@ -65,7 +65,8 @@ class Partition(C.Structure):
 class Profile(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("probe_ms", C.c_double),
                 ("probe_launches", C.c_uint64), ("scan_ms", C.c_double),
-                ("scan_launches", C.c_uint64), ("switched_queries", C.c_uint64)]
+                ("scan_launches", C.c_uint64), ("switched_queries", C.c_uint64),
+                ("rerun_queries", C.c_uint64), ("rerun_ms", C.c_double)]
 
 
 # every symbol include/mihg.h declares: (name, restype, argtypes)

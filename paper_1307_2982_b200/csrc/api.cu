@@ -382,6 +382,8 @@ void mihg_profile_reset(void) {
   p.probe_ms = p.scan_ms = 0;
   p.probe_launches = p.scan_launches = 0;
   p.switched_queries = 0;
+  p.rerun_queries = 0;
+  p.rerun_ms = 0;
 }
 
 int mihg_profile_read(mihg_profile* out) {
@@ -392,6 +394,8 @@ int mihg_profile_read(mihg_profile* out) {
   out->scan_ms = p.scan_ms;
   out->scan_launches = p.scan_launches;
   out->switched_queries = p.switched_queries;
+  out->rerun_queries = p.rerun_queries;
+  out->rerun_ms = p.rerun_ms;
   return MIHG_OK;
 }
 

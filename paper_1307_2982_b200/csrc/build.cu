@@ -63,6 +63,21 @@ int device_sm_count() {
   return sms;
 }
 
+// The stream-ordered pool returns freed memory to the driver at every synchronisation by
+// default, so a step's temporaries (selection buffers, re-run buffers) would be re-mapped on each
+// call. Keep up to MIHG_POOL_KEEP_MB (default 16 GB) cached in the device's default pool.
+void configure_mempool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  const char* e = std::getenv("MIHG_POOL_KEEP_MB");
+  const uint64_t keep = uint64_t(e ? std::strtoull(e, nullptr, 10) : 16384) << 20;
+  cudaMemPool_t pool;
+  MIHG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t v = keep;
+  MIHG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &v));
+  done[device] = true;
+}
+
 void validate_partition(uint32_t bits, uint32_t m, const uint32_t* lengths,
                         const uint32_t* positions) {
   if (bits == 0 || bits > kMaxCodeBits) throw InvalidArgument("Partition: bad width");
@@ -380,6 +395,7 @@ Index* build_index(const uint64_t* codes, bool codes_on_device, uint64_t n, uint
     throw InvalidArgument("shard id range exceeds 2^32");
 
   MIHG_CUDA(cudaSetDevice(device));
+  configure_mempool(device);
   auto idx = std::make_unique<Index>();
   idx->device = device;
   MIHG_CUDA(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking));

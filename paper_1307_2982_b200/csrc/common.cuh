@@ -192,6 +192,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 inline uint32_t ceil_div_u32(uint64_t a, uint64_t b) { return uint32_t((a + b - 1) / b); }
 
 int device_sm_count();
+void configure_mempool(int device);  // keep freed stream-ordered memory cached (build.cu)
 void set_last_error(const std::string& msg);
 
 // Live per-kernel timing (CUDA events on the launching stream), enabled by mihg_profile_enable.
@@ -202,6 +203,8 @@ struct ProfileState {
   double scan_ms = 0;
   uint64_t scan_launches = 0;
   uint64_t switched_queries = 0;  // queries finished by the exhaustive scan (hybrid switch)
+  uint64_t rerun_queries = 0;     // queries whose candidate buffer overflowed (exact re-run pass)
+  double rerun_ms = 0;            // host wall time of the re-run passes
 };
 ProfileState& profile();  // thread-local message behind mihg_last_error()
 

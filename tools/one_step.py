@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--nq", type=int, default=0)
+    ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--traced", action="store_true")
     a = ap.parse_args()
     import torch
@@ -26,6 +27,8 @@ def main():
     cfg = dict(bench.CONFIGS[a.config])
     if a.nq:
         cfg["nq"] = a.nq
+    if a.k:
+        cfg["k"] = a.k
     dev = torch.device("cuda", 0)
     L = _lib.lib()
     codes = bench.make_codes_device(cfg, 0, cfg["n"], cfg["db_seed"], torch, dev, L)

@@ -313,6 +313,10 @@ def main():
         from paper_1307_2982_b200.shard import nccl_allreduce
 
         partition = (world, rank, nccl_allreduce())
+    elif world > 1 and args.method == "mih":  # id-range shards with global stopping (§8e refinement 1)
+        from paper_1307_2982_b200.shard import nccl_allreduce
+
+        partition = (world, rank, nccl_allreduce(), True)
 
     def step(qptr=None):
         qptr = qptr or queries.data_ptr()

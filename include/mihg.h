@@ -150,13 +150,22 @@ int mihg_range_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint
  * 1: u64) in place across ranks, ordered on `stream`, and return 0 (e.g. an NCCL all-reduce);
  * it is called once per radius round with the per-query histograms, so all ranks apply the
  * reference's stopping rule to the global counts. Outputs are the rank's LOCAL top-k (padded
- * with 0xFFFFFFFF): all-gather them and merge with mihg_merge_topk_device. Traces are global. */
+ * with 0xFFFFFFFF): all-gather them and merge with mihg_merge_topk_device. Traces are global.
+ *
+ * id_shards = 1 selects the id-range layout instead (refinement 1 "global
+ * stopping"): each rank's index holds only its own id range (built with id_base), every rank
+ * probes every ring, and the same per-round histogram all-reduce makes all shards stop at the
+ * GLOBAL d_k instead of their larger local d_k. count may be any value >= 1; the hybrid
+ * scan switch is off (ranks' shard sizes may differ, the decision must be collective).
+ * Traces: candidates/unique are summed over shards (= the single-index trace), lookups and
+ * final_radius are every shard's own (= the single-index values). */
 typedef int (*mihg_allreduce_fn)(void* user, void* dev_ptr, uint64_t count, int dtype, void* stream);
 typedef struct mihg_partition {
   uint32_t count;
   uint32_t rank;
   mihg_allreduce_fn allreduce;
   void* user;
+  uint32_t id_shards; /* 0: probe-space partition of a replicated index; 1: id-range shards */
 } mihg_partition;
 int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
                                uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces,

@@ -276,6 +276,7 @@ int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint6
       pt.rank = part->rank;
       pt.allreduce = part->allreduce;
       pt.user = part->user;
+      pt.id_shards = part->id_shards != 0;
     }
     mihg::KnnOptions opt;
     opt.part = part ? &pt : nullptr;

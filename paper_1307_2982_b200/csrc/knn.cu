@@ -991,7 +991,10 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
 
   ProbeArgs p = make_probe_args(idx, ws, d_q);
   uint64_t part_lo = 0, part_hi = idx.n;  // id range this rank scans if queries switch to K6
-  if (part) {
+  if (part && part->id_shards) {  // every shard probes every ring; only the counts are global
+    if (part->rank >= part->count) throw InvalidArgument("partitioned knn: rank must be < count");
+    if (ws.hist_g.size() < nq * b1) ws.hist_g = DeviceBuffer<uint32_t>(ws.nq_cap * b1, st);
+  } else if (part) {
     uint32_t bits = 0;
     while ((1u << bits) < part->count) ++bits;
     if ((1u << bits) != part->count || part->rank >= part->count)
@@ -1011,7 +1014,8 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   uint32_t* act_out = ws.act1.get();
   uint64_t nact = nq;
   uint64_t acc = 0;
-  const double alpha = (d_tr || (part && part_hi - part_lo < k)) ? 0.0 : hybrid_alpha();
+  const double alpha =
+      (d_tr || (part && (part->id_shards || part_hi - part_lo < k))) ? 0.0 : hybrid_alpha();
   const double scan_pairs = double(idx.n) * idx.W, probe_pairs = 36.0 + 15.0 * (idx.W - 1);
   uint32_t* switched = nullptr;
   uint64_t nswitched = 0;

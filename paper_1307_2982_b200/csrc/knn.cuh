@@ -19,6 +19,7 @@ struct Partition {
   uint32_t count = 1, rank = 0;
   int (*allreduce)(void* user, void* dev_ptr, uint64_t count, int dtype, void* stream) = nullptr;
   void* user = nullptr;
+  bool id_shards = false;  // id-range shards with global stopping (no probe split)
 };
 
 struct KnnOptions {

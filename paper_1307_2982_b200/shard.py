@@ -110,16 +110,23 @@ class ShardedKnn:
         return cls(local, index.size(), group)
 
     @classmethod
-    def from_index(cls, index, group=None):
-        """Wrap a local ``MihIndex`` (built with id_base = shard start) whose queries live on the GPU."""
+    def from_index(cls, index, group=None, global_stopping: bool = True):
+        """Wrap a local ``MihIndex`` (built with id_base = shard start) whose queries live on the GPU.
+        With ``global_stopping`` (SURVEY §8e refinement 1) the per-round histograms are summed
+        over the group so every shard stops at the global d_k, not its larger local d_k."""
         import torch
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        part = (world, rank, nccl_allreduce(group), True) if (global_stopping and world > 1) else None
 
         def local(queries, k):
             nq = queries.shape[0]
             ids = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
             d = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
             index.knn_search_device(queries.data_ptr(), nq, k, ids.data_ptr(), d.data_ptr(),
-                                    stream=torch.cuda.current_stream(queries.device).cuda_stream)
+                                    stream=torch.cuda.current_stream(queries.device).cuda_stream,
+                                    partition=part)
             return ids, d
 
         return cls(local, index.size(), group)

@@ -119,13 +119,16 @@ __device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint
     lo = hi = 0;
     return;
   }
-  if (y.w != kNoEscape) {
+  const uint64_t below = (uint64_t(1) << tt) - 1u;
+  // Escaped block (some bucket holds >= 7 entries, stored as count 7): the planes are still exact
+  // for every bucket with count <= 6, so the escape record is read only when this bucket or one
+  // below it is saturated (the clusters the probes visit are where blocks escape).
+  if (y.w != kNoEscape && (c == 7u || (p0 & p1 & p2 & below) != 0)) {
     const uint32_t* e = t.esc + uint64_t(y.w) * 65u + tt;
     lo = __ldg(e);
     hi = __ldg(e + 1);
     return;
   }
-  const uint64_t below = (uint64_t(1) << tt) - 1u;
   lo = y.z + __popcll(p0 & below) + 2u * __popcll(p1 & below) + 4u * __popcll(p2 & below);
   hi = lo + c;
 }

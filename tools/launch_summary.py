@@ -15,7 +15,8 @@ def main(path, top=25):
     for r in rows[h + 1:]:
         if len(r) <= vi:
             continue
-        name = r[ki].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
+        name = r[ki].replace("(anonymous namespace)", "").replace("<unnamed>", "").replace("void ", "")
+        name = name.split("(")[0].split("<")[0].split("::")[-1] or r[ki][:60]
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     tot = sum(v[1] for v in agg.values()) or 1.0

@@ -462,7 +462,24 @@ def main():
     # per GPU: a probe-partitioned rank moves 1/N of the step's algorithmic bytes
     achieved = alg_bytes / (world if probe_part else 1) / (probe_ms / 1000.0) / 1e9 if probe_ms > 0 else 0.0
     switched = (prof1.switched_queries - prof0.switched_queries) / args.steps
-    if args.method == "scan" or switched >= 0.5 * nq:
+    scan_ms_step = (prof1.scan_ms - prof0.scan_ms) / args.steps
+    scanned_q = nq if args.method == "scan" else switched
+    if (args.method == "scan" or switched >= 0.5 * nq) and L.mihg_scan_kernel_for(bits) == 1:
+        # K7 (tcgen05 kind::i8): one useful MAC per code bit per (query, code) pair; the peak is the
+        # dense int8 rate = 2x the measured cuBLAS bf16 burst (MEASURED_PEAKS.json), else 2x fallback
+        bf16 = float(peaks.get("bf16_tflops", 0) or 0)
+        i8_peak = 2.0 * (bf16 if bf16 > 0 else 1590.0)
+        t_s = (scan_ms_step if scan_ms_step > 0 else ms_per_step) / 1000.0
+        ops = 2.0 * scanned_q * (hi - lo) * bits
+        roofline = {"bound": "tensor", "achieved": ops / t_s / 1e12, "peak": i8_peak, "unit": "TOPS",
+                    "frac": ops / t_s / 1e12 / i8_peak, "traffic": None, "kernel": "tc_scan_kernel",
+                    "peak_source": ("2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)" if bf16 > 0
+                                    else "2x fallback 1590 TF/s bf16"),
+                    "scan_kernel_ms_per_step": scan_ms_step,
+                    "scanned_queries_per_step": scanned_q,
+                    "note": ("exhaustive K7 path" if args.method == "scan" else
+                             "hybrid: %d of %d queries per step finished by the tensor-core scan" % (switched, nq))}
+    elif args.method == "scan" or switched >= 0.5 * nq:
         # K6 is POPC-bound: n*W popc64 = 2*n*W POPC32 per query; peak = 16 POPC/clk/SM measured
         # 4.56e12/s at 1.925 GHz (tools/probe/ubench.cu), scaled to the sampled SM clock.
         pc_peak = 4.56e12 * ((clk.get("sm_mhz") or 1925.0) / 1925.0)

@@ -181,6 +181,14 @@ int mihg_scan_knn_raw_device(const uint64_t* d_codes, uint64_t n, uint32_t bits,
                              const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
                              uint32_t* d_dists, void* stream);
 
+/* Exhaustive kernel behind the scan entry points: K7 (tcgen05 int8 tensor-core scan, codes of at
+ * most 256 bits; the default there) or K6 (POPC pipe). Results are identical. Environment
+ * MIHG_SCAN_KERNEL=popc|tc overrides the choice. Returns 0 = K6, 1 = K7 for a code width. */
+int mihg_scan_kernel_for(uint32_t bits);
+/* Test hook: every K7 distance of nq queries x n codes (device int32 [nq][n]), n*nq small. */
+int mihg_tc_distances_device(const uint64_t* d_codes, uint64_t n, uint32_t bits,
+                             const uint64_t* d_queries, uint64_t nq, int32_t* d_out, void* stream);
+
 /* Exact k-way merge of G per-shard top-k lists: inputs [G][nq][k_in] device
  * arrays (dist 0xFFFFFFFF = padding), output the k_out smallest (dist, id) per query. */
 int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint32_t G, uint64_t nq,

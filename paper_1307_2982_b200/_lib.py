@@ -99,6 +99,9 @@ SYMBOLS = [
     ("mihg_scan_knn_raw_device", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
                                            C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p,
                                            C.c_void_p, C.c_void_p]),
+    ("mihg_scan_kernel_for", C.c_int, [C.c_uint32]),
+    ("mihg_tc_distances_device", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint64,
+                                           C.c_void_p, C.c_void_p]),
     ("mihg_merge_topk_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64,
                                          C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),

@@ -363,6 +363,21 @@ int mihg_scan_knn_raw_device(const uint64_t* d_codes, uint64_t n, uint32_t bits,
   });
 }
 
+int mihg_scan_kernel_for(uint32_t bits) {
+  return mihg::scan_kernel_for(bits) == mihg::ScanKernel::Tensor ? 1 : 0;
+}
+
+int mihg_tc_distances_device(const uint64_t* d_codes, uint64_t n, uint32_t bits,
+                             const uint64_t* d_queries, uint64_t nq, int32_t* d_out, void* stream) {
+  return guarded([&] {
+    if (n == 0 || nq == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    mihg::DeviceBuffer<uint32_t> di(nq, st), dd(nq, st);
+    mihg::tc_scan_knn_device(d_codes, n, bits, 0, d_queries, nq, 1, di.get(), dd.get(), st, d_out);
+    MIHG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint32_t G, uint64_t nq,
                            uint32_t k_in, uint32_t k_out, uint32_t* d_out_ids,
                            uint32_t* d_out_dists, void* stream) {

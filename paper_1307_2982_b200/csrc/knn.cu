@@ -877,6 +877,19 @@ double hybrid_alpha() {
   return v;
 }
 
+// Exhaustive-scan cost per (query, code) pair in the same 64-bit-popcount units: W on the POPC
+// pipe (K6); the tensor-core scan (K7) is cheaper by the measured B200 ratio of the two kernels'
+// pair rates (tools/bench_tcscan.py; MIHG_TC_SPEEDUP overrides).
+double scan_cost_per_code(uint32_t bits) {
+  const uint32_t W = words_per_code(bits);
+  if (scan_kernel_for(bits) != ScanKernel::Tensor) return W;
+  const char* e = std::getenv("MIHG_TC_SPEEDUP");
+  // measured pair rates (tools/bench_tcscan.py, n = 1e8, 1e4 queries): K7 ~3.3e12 pairs/s at every
+  // width (accumulator-drain bound); K6 1.95e12 (W=1) ... 5.3e11 (W=4) pairs/s
+  const double f = e ? std::atof(e) : (W == 1 ? 1.7 : W == 2 ? 3.0 : W == 3 ? 4.5 : 6.0);
+  return W / f;
+}
+
 ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   ProbeArgs p{};
   p.codes = idx.codes.get();
@@ -1016,7 +1029,8 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   uint64_t acc = 0;
   const double alpha =
       (d_tr || (part && (part->id_shards || part_hi - part_lo < k))) ? 0.0 : hybrid_alpha();
-  const double scan_pairs = double(idx.n) * idx.W, probe_pairs = 36.0 + 15.0 * (idx.W - 1);
+  const double scan_pairs = double(idx.n) * scan_cost_per_code(idx.bits),
+               probe_pairs = 36.0 + 15.0 * (idx.W - 1);
   uint32_t* switched = nullptr;
   uint64_t nswitched = 0;
   for (uint32_t r = 0; nact > 0; ++r) {

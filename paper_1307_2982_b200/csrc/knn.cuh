@@ -44,6 +44,15 @@ void scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_
                      const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
                      uint32_t* d_dists, cudaStream_t st);
 
+// K7: the same exhaustive k-NN on the tensor cores (tcscan.cu), codes of 1..256 bits. d_dump
+// (tests only, nullable): every distance, nq x n row-major.
+bool tc_scan_supported(uint32_t bits);
+void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                        const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                        uint32_t* d_dists, cudaStream_t st, int32_t* d_dump);
+enum class ScanKernel { Popc, Tensor };
+ScanKernel scan_kernel_for(uint32_t bits);
+
 // k-way merge of G per-shard sorted (dist, id) lists per query (exact: smallest keys win).
 void merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint32_t G, uint64_t nq,
                        uint32_t k_in, uint32_t k_out, uint32_t* d_out_ids, uint32_t* d_out_dists,

@@ -12,9 +12,11 @@
 // at tau keep the earliest = smallest ids) and tau tightens. A final per-query selection over
 // all warp lists gives the exact global top-k.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "knn.cuh"
+#include "scanlist.cuh"
 #include "select.cuh"
 
 namespace mihg {
@@ -36,57 +38,6 @@ struct ScanArgs {
   uint32_t* counts;      // [q][split*8 + warp]
   uint32_t slots;        // nsplit * kScanWarps
 };
-
-// In-place exact top-k of a warp's list (ids ascending in list order); returns the new bound.
-__device__ __noinline__ uint32_t compact_list(uint64_t* list, uint32_t& cnt, uint32_t tau, uint32_t k,
-                                 uint32_t* hist) {
-  const uint32_t lane = threadIdx.x & 31;
-  MIHG_DASSERT(tau < 4097);
-  for (uint32_t d = lane; d <= tau; d += 32) hist[d] = 0;
-  __syncwarp();
-  for (uint32_t i = lane; i < cnt; i += 32) atomicAdd(&hist[uint32_t(list[i] >> 32)], 1u);
-  __syncwarp();
-  uint32_t run = 0, newtau = tau, before = 0;
-  bool found = false;
-  for (uint32_t d0 = 0; d0 <= tau && !found; d0 += 32) {
-    const uint32_t d = d0 + lane;
-    uint32_t v = d <= tau ? hist[d] : 0;
-    const uint32_t own = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(~0u, v, o);
-      if (lane >= o) v += y;
-    }
-    const uint32_t ok = __ballot_sync(~0u, d <= tau && run + v >= k);
-    if (ok) {
-      const int src = __ffs(ok) - 1;
-      newtau = d0 + src;
-      before = run + __shfl_sync(~0u, v - own, src);
-      found = true;
-    }
-    run += __shfl_sync(~0u, v, 31);
-  }
-  if (!found) return tau;  // fewer than k entries: nothing to drop
-  const uint32_t need_eq = k - before;
-  uint32_t wpos = 0, eq_seen = 0;
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const uint64_t key = i < cnt ? list[i] : ~0ull;
-    const uint32_t d = uint32_t(key >> 32);
-    const bool eq = i < cnt && d == newtau;
-    const uint32_t eqbal = __ballot_sync(~0u, eq);
-    const bool keep = (i < cnt && d < newtau) ||
-                      (eq && eq_seen + __popc(eqbal & lanemask_lt()) < need_eq);
-    const uint32_t bal = __ballot_sync(~0u, keep);
-    __syncwarp();
-    if (keep) list[wpos + __popc(bal & lanemask_lt())] = key;
-    __syncwarp();
-    wpos += __popc(bal);
-    eq_seen += __popc(eqbal);
-  }
-  cnt = wpos;
-  return newtau;
-}
 
 template <int W, int QT>
 __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanArgs a) {
@@ -167,30 +118,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_kernel(ScanArgs a) {
     if (q0 + t < a.nq && lane == 0) a.counts[(q0 + t) * a.slots + slot] = cnt[t];
 }
 
-// Gather the per-warp lists of one query into a contiguous segment (one CTA per query).
-__global__ void gather_lists_kernel(const uint64_t* __restrict__ lists,
-                                    const uint32_t* __restrict__ counts, uint32_t slots, uint32_t L,
-                                    uint64_t* __restrict__ out, uint32_t* __restrict__ out_count) {
-  __shared__ uint32_t s_off[1025];
-  const uint64_t q = blockIdx.x;
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (uint32_t s = 0; s < slots; ++s) {
-      s_off[s] = acc;
-      acc += counts[q * slots + s];
-    }
-    s_off[slots] = acc;
-    out_count[q] = acc;
-  }
-  __syncthreads();
-  const uint64_t obase = q * uint64_t(slots) * L;
-  for (uint32_t s = threadIdx.x >> 5; s < slots; s += blockDim.x >> 5) {
-    const uint32_t c = s_off[s + 1] - s_off[s];
-    const uint64_t* src = lists + (q * slots + s) * uint64_t(L);
-    for (uint32_t i = threadIdx.x & 31; i < c; i += 32) out[obase + s_off[s] + i] = src[i];
-  }
-}
-
 template <int W, int QT>
 void launch_scan(ScanArgs a, cudaStream_t st) {
   const uint32_t tiles = uint32_t((a.nq + QT - 1) / QT);
@@ -203,10 +130,23 @@ void launch_scan(ScanArgs a, cudaStream_t st) {
 
 }  // namespace
 
+// Which exhaustive kernel serves scan_knn: K7 (tensor cores, tcscan.cu) for codes up to 256 bits,
+// K6 (POPC pipe) otherwise. MIHG_SCAN_KERNEL=popc|tc forces one (A/B measurement, tests).
+ScanKernel scan_kernel_for(uint32_t bits) {
+  const char* e = std::getenv("MIHG_SCAN_KERNEL");
+  if (e && e[0] == 'p') return ScanKernel::Popc;
+  if (e && e[0] == 't' && tc_scan_supported(bits)) return ScanKernel::Tensor;
+  return tc_scan_supported(bits) ? ScanKernel::Tensor : ScanKernel::Popc;
+}
+
 void scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
                      const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
                      uint32_t* d_dists, cudaStream_t st) {
   if (k > n) throw InvalidArgument("scan_knn: k exceeds database size");
+  if (scan_kernel_for(bits) == ScanKernel::Tensor) {
+    tc_scan_knn_device(d_codes, n, bits, id_base, d_queries, nq, k, d_ids, d_dists, st, nullptr);
+    return;
+  }
   if (nq == 0 || k == 0) return;
   const uint32_t nw = words_per_code(bits);
   const int QT = nw <= 2 ? 16 : (nw <= 4 ? 8 : 4);

@@ -1,0 +1,588 @@
+// Exhaustive batched k-NN on the 5th-generation tensor cores (K7): scan_knn (scan.hpp:43-68) as
+// an integer GEMM. sm_100a has no binary MMA, but the int8 tcgen05 MMA is
+// exact for 0/1 data: with the database bit x_i in {0, 1} (u8) and the query bit as
+// a_i = 1 - 2 q_i in {+1, -1} (s8),
+//     sum_i x_i a_i = popc(x) - 2 popc(x & q) = d(q, x) - popc(q),
+// so the s32 accumulator is the Hamming distance up to the per-query constant popc(q). One
+// M=128 x N=256 x K=32 instruction evaluates 32768 (query, code) pairs on 32 bits; the POPC pipe
+// needs 2048 instructions for the same work.
+//
+// CTA = 128 queries (TMEM lanes) x one id chunk of the database, one CTA per SM, warp-specialised:
+//   warps 0-7   epilogue: thread (warp % 4, lane) owns query row 32 (warp % 4) + lane; group
+//               g = warp / 4 drains columns [64 g, 64 g + 64) of every 128-code tile and keeps its
+//               own candidate list per query (id order, compacted to the exact top-k when it reaches
+//               2k entries; scanlist.cuh, as in K6), under a bound shared by all lists of the query.
+//   warps 8-11  producers: each thread takes one code per tile from the raw ring and expands it
+//               to K bytes of 0/1 in the no-swizzle K-major canonical layout of the B operand
+//               (8-row x 16-byte core matrices).
+//   warp 12     TMEM allocation and the single-thread tcgen05.mma issue.
+//   warp 13     loader: one thread keeps kRaw raw code tiles in flight from HBM/L2 into shared
+//               memory with 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx) — the
+//               latency of the shared (L2-resident) chunk is far longer than a tile's MMA.
+// Pipelines: B stages full/empty (producers <-> MMA, mbarriers; tcgen05.commit frees a stage) and
+// four TMEM accumulators of 128 columns (MMA <-> epilogue), so the MMA runs up to four tiles
+// ahead of the accumulator drain.
+// The per-query selection over the lists is K6's (gather + select_topk), so ties resolve to the
+// smaller id exactly as scan.hpp:24-26.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "knn.cuh"
+#include "scanlist.cuh"
+#include "select.cuh"
+
+namespace mihg {
+
+namespace {
+
+constexpr int kTcM = 128;        // queries per CTA (TMEM lanes)
+constexpr int kTcN = 128;        // codes per tile (MMA N)
+constexpr int kAcc = 4;          // TMEM accumulators of kTcN columns (512 columns allocated)
+constexpr int kEpiGroups = 4;    // epilogue groups of 4 warps; group g drains columns [32 g, 32 g + 32)
+constexpr int kEpiCols = kTcN / kEpiGroups;
+constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kProdWarps = 4;    // 128 producer threads: one code each per tile
+constexpr int kRaw = 16;         // raw code tiles in flight (TMA bulk ring)
+constexpr int kTcThreads = (kEpiWarps + kProdWarps + 2) * 32;
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;
+constexpr int kLoadWarp = kMmaWarp + 1;
+
+struct TcArgs {
+  const uint64_t* codes;
+  uint64_t n;
+  uint32_t bits, k;
+  const uint64_t* queries;
+  uint64_t nq;
+  uint32_t qtiles;
+  uint64_t chunk;  // codes per chunk (multiple of kTcN)
+  uint32_t L;
+  uint64_t* lists;   // [q][slot][L], slot = chunk * kEpiGroups + group
+  uint32_t* counts;  // [q][slot]
+  uint32_t slots;
+  int32_t* dump;     // debug: nq x n distances (tests only), or nullptr
+  uint32_t* gbound;  // [q]: smallest k-th distance proven by any list of the query (0xFFFFFFFF = none)
+  unsigned long long* prof;  // debug (MIHG_TC_PROF=1): [warp][8] cycle counters summed over CTAs
+  uint32_t experiment;  // timing experiments only (MIHG_TC_EXPERIMENT): 1 = group 1 skips its TMEM load
+  uint32_t desc_swap;  // debug (MIHG_TC_DESC_SWAP=1): exchange LBO and SBO in the descriptors
+};
+
+// ---- PTX wrappers (tcgen05 / mbarrier) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// test_wait spin (no suspend): experiment 64
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8 (A signed, B unsigned, s32 accumulate)
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, K-major, no swizzle: core matrices of 8 rows x 16 bytes stored
+// contiguously; LBO = byte step between K-adjacent core matrices, SBO = between 8-row groups.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((addr & 0x3FFFFu) >> 4) | (uint64_t(lbo >> 4) << 16) | (uint64_t(sbo >> 4) << 32) |
+         (uint64_t(1) << 46);  // version 1 (tcgen05), base offset 0, layout SWIZZLE_NONE
+}
+
+// Instruction descriptor: kind::i8, D = s32, A = s8 (signed), B = u8, both K-major, M x N.
+constexpr uint32_t tc_idesc(uint32_t M, uint32_t N) {
+  return (2u << 4) | (1u << 7) | (0u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+#define TC_R8(i) "=r"(v[i + 0]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), \
+                 "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+// 32 TMEM lanes x 32 consecutive 32-bit columns -> 32 registers per thread (lane = thread).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : TC_R8(0), TC_R8(8), TC_R8(16), TC_R8(24)
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+#undef TC_R8
+
+// 4 bits -> 4 bytes of 0/1 (bit i -> byte i)
+__device__ __forceinline__ uint32_t spread4(uint32_t x) { return (x * 0x00204081u) & 0x01010101u; }
+
+// byte offset of (row r, 16-byte K chunk c) in a no-swizzle K-major operand with KB bytes per row
+template <int KB>
+__device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t c) {
+  return (r >> 3) * (KB * 8) + c * 128 + (r & 7) * 16;
+}
+
+// The 16-byte-aligned part of a raw tile's code bytes (TMA bulk copies need 16-byte alignment and
+// size): it starts `skip` bytes into the tile and is `bytes` long; codes outside it (a misaligned
+// head, an odd tail) are read with plain loads.
+template <int W>
+__device__ __forceinline__ void raw_span(const uint64_t* codes, uint64_t id0, uint64_t hi, uint32_t& skip,
+                                         uint32_t& bytes) {
+  const uintptr_t s = reinterpret_cast<uintptr_t>(codes + id0 * W);
+  const uintptr_t e = reinterpret_cast<uintptr_t>(codes + min(hi, id0 + kTcN) * W);
+  const uintptr_t s16 = (s + 15) & ~uintptr_t(15), e16 = e & ~uintptr_t(15);
+  skip = uint32_t(s16 - s);
+  bytes = e16 > s16 ? uint32_t(e16 - s16) : 0u;
+}
+
+template <int KB>
+struct TcCfg {
+  static constexpr int W = KB / 64;
+  static constexpr uint32_t kA = kTcM * KB;
+  static constexpr uint32_t kB = kTcN * KB;
+  static constexpr int kStages = KB <= 64 ? 8 : (KB <= 128 ? 6 : (KB <= 192 ? 4 : 3));
+  static constexpr uint32_t kRawBytes = kTcN * W * 8;  // one raw tile of packed codes
+  static constexpr uint32_t kSmem = 1024 + kA + kStages * kB + kRaw * kRawBytes;  // + barriers/hist
+};
+
+template <int KB, bool kDump>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
+  using Cfg = TcCfg<KB>;
+  constexpr int W = Cfg::W;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + Cfg::kA;
+  uint8_t* sRaw = sB + S * Cfg::kB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRaw + kRaw * Cfg::kRawBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + kAcc;
+  uint64_t* rfull = bars + 2 * S + 2 * kAcc;
+  uint64_t* rempty = rfull + kRaw;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + kRaw);
+  uint32_t* hist_all = tmem_slot + 4;  // kEpiWarps * (bits + 1)
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool spin = (a.experiment & 64) != 0;
+  unsigned long long wcyc[4] = {0, 0, 0, 0};
+  auto wait_k = [&](uint64_t* bar, uint32_t parity, int kind) {
+    const unsigned long long c0 = a.prof ? clock64() : 0;
+    if (spin) mbar_spin(bar, parity);
+    else mbar_wait(bar, parity);
+    if (a.prof) wcyc[kind] += clock64() - c0;
+  };
+  auto wait = [&](uint64_t* bar, uint32_t parity) { wait_k(bar, parity, 0); };
+  const unsigned long long t_start = clock64();
+  const uint32_t qtile = blockIdx.x % a.qtiles, chunk = blockIdx.x / a.qtiles;
+  const uint64_t q0 = uint64_t(qtile) * kTcM;
+  const uint64_t lo = uint64_t(chunk) * a.chunk;
+  const uint64_t hi = min(a.n, lo + a.chunk);
+  const uint32_t T = uint32_t((hi - lo + kTcN - 1) / kTcN);
+
+  if (warp == kMmaWarp) {
+    if (lane == 0) {
+      for (int s = 0; s < S; ++s) {
+        mbar_init(full + s, kProdWarps);
+        mbar_init(empty + s, 1);
+      }
+      for (int b = 0; b < kAcc; ++b) {
+        mbar_init(tfull + b, 1);
+        mbar_init(tempty + b, kEpiWarps);
+      }
+      for (int r = 0; r < kRaw; ++r) {
+        mbar_init(rfull + r, 1);
+        mbar_init(rempty + r, kProdWarps);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // A operand: the 128 queries of the tile as +1 (bit 0) / -1 (bit 1) bytes; padding rows zero
+  for (uint32_t u = threadIdx.x; u < uint32_t(kTcM) * (KB / 16); u += kTcThreads) {
+    const uint32_t r = u / (KB / 16), c = u % (KB / 16);
+    const uint64_t q = q0 + r;
+    uint4 o = make_uint4(0, 0, 0, 0);
+    if (q < a.nq) {
+      const uint32_t h = uint32_t(__ldg(a.queries + q * W + (c >> 2)) >> ((c & 3) * 16)) & 0xFFFFu;
+      o.x = (spread4(h & 0xF) * 0xFEu) ^ 0x01010101u;
+      o.y = (spread4((h >> 4) & 0xF) * 0xFEu) ^ 0x01010101u;
+      o.z = (spread4((h >> 8) & 0xF) * 0xFEu) ^ 0x01010101u;
+      o.w = (spread4(h >> 12) * 0xFEu) ^ 0x01010101u;
+    }
+    *reinterpret_cast<uint4*>(sA + core_off<KB>(r, c)) = o;
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kMmaWarp) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
+      const uint32_t a_addr = smem_u32(sA), b_addr = smem_u32(sB);
+      for (uint32_t t = 0; t < T; ++t) {
+        const uint32_t s = t % S, ph = (t / S) & 1, b = t % kAcc, bph = (t / kAcc) & 1;
+        wait_k(tempty + b, bph ^ 1, 0);
+        wait_k(full + s, ph, 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < KB / 32; ++kk) {
+          const uint32_t lbo = a.desc_swap ? KB * 8 : 128, sbo = a.desc_swap ? 128 : KB * 8;
+          const uint64_t ad = smem_desc(a_addr + kk * 256, lbo, sbo);
+          const uint64_t bd = smem_desc(b_addr + s * Cfg::kB + kk * 256, lbo, sbo);
+          if (!(a.experiment & 2)) tc_mma_i8(tmem + b * kTcN, ad, bd, idesc, kk > 0);
+        }
+        tc_commit(empty + s);
+        tc_commit(tfull + b);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kLoadWarp) {
+    // ===== loader: raw code tiles -> shared memory (TMA bulk copies) =====
+    if (lane == 0) {
+      for (uint32_t t = 0; t < T; ++t) {
+        const uint32_t r = t % kRaw;
+        wait(rempty + r, ((t / kRaw) & 1) ^ 1);
+        uint32_t skip, bytes;
+        raw_span<W>(a.codes, lo + uint64_t(t) * kTcN, hi, skip, bytes);
+        const uint32_t bar = smem_u32(rfull + r);
+        if (bytes) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sRaw + r * Cfg::kRawBytes)),
+              "l"(reinterpret_cast<const uint8_t*>(a.codes + (lo + uint64_t(t) * kTcN) * W) + skip), "r"(bytes),
+              "r"(bar)
+              : "memory");
+        } else {
+          mbar_arrive(rfull + r);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kEpiWarps) {
+    // ===== producers: raw code -> 0/1 bytes =====
+    const uint32_t p = threadIdx.x - kEpiWarps * 32;  // code row within the tile
+    for (uint32_t t = 0; t < T; ++t) {
+      const uint32_t s = t % S, ph = (t / S) & 1, r = t % kRaw;
+      const uint64_t id = lo + uint64_t(t) * kTcN + p;
+      uint32_t skip, tbytes;
+      raw_span<W>(a.codes, lo + uint64_t(t) * kTcN, hi, skip, tbytes);
+      wait_k(rfull + r, (t / kRaw) & 1, 0);
+      uint64_t cur[W];
+      if (p * W * 8 >= skip && (p + 1) * W * 8 <= skip + tbytes) {
+        const uint64_t* src = reinterpret_cast<const uint64_t*>(sRaw + r * Cfg::kRawBytes + p * W * 8 - skip);
+#pragma unroll
+        for (int w = 0; w < W; ++w) cur[w] = src[w];
+      } else if (id < hi) {  // tail of the last tile (not a multiple of 16 bytes)
+#pragma unroll
+        for (int w = 0; w < W; ++w) cur[w] = __ldg(a.codes + id * W + w);
+      } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) cur[w] = 0;
+      }
+      if (a.experiment & 16) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) cur[w] = 0;
+      }
+      wait_k(empty + s, ph ^ 1, 1);
+      uint8_t* dst = sB + s * Cfg::kB;
+      if (!(a.experiment & 4))
+#pragma unroll
+        for (int c = 0; c < KB / 16; ++c) {
+          const uint32_t h = uint32_t(cur[c >> 2] >> ((c & 3) * 16)) & 0xFFFFu;
+          const uint4 o = make_uint4(spread4(h & 0xF), spread4((h >> 4) & 0xF), spread4((h >> 8) & 0xF),
+                                     spread4(h >> 12));
+          *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c)) = o;
+        }
+      if (!(a.experiment & 32)) fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(full + s);
+        mbar_arrive(rempty + r);  // the raw words were consumed by the expansion above
+      }
+    }
+  } else {
+    // ===== epilogue: TMEM -> registers -> bound test -> candidate list =====
+    // Accept bound per query: min(own, shared). own = bits until the list is first compacted, then
+    // (its k-th distance) - 1: a later id at that distance ranks below all k kept entries.
+    // shared = gbound[q], the smallest k-th distance any list of this query has proven (atomicMin
+    // after each compaction); ties at it are still accepted (another slot may hold smaller ids).
+    const uint32_t g = warp >> 2, quad = warp & 3;
+    const uint32_t row = quad * 32 + lane;
+    const uint64_t q = q0 + row;
+    const bool qvalid = q < a.nq;
+    const uint64_t* qp = a.queries + (qvalid ? q : 0) * W;
+    int32_t pq = 0;
+    if (qvalid)
+      for (int w = 0; w < W; ++w) pq += __popcll(__ldg(qp + w));
+    int32_t own = qvalid ? int32_t(a.bits) : -1;
+    uint32_t cnt = 0;
+    const uint32_t slot = chunk * kEpiGroups + g;
+    uint64_t* list = a.lists + ((qvalid ? q : 0) * a.slots + slot) * uint64_t(a.L);
+    uint32_t* hist = hist_all + warp * (a.bits + 1);
+    const uint32_t taddr0 = tmem + ((quad * 32) << 16) + g * kEpiCols;
+    // the shared bound is refreshed every 4 tiles from a load issued 4 tiles earlier (L2 latency)
+    uint32_t gb_next = qvalid ? __ldcg(a.gbound + q) : 0u;
+    int32_t shared_b = qvalid ? int32_t(a.bits) : -1;
+    for (uint32_t t = 0; t < T; ++t) {
+      const uint32_t b = t % kAcc, bph = (t / kAcc) & 1;
+      if ((t & 3) == 0 && qvalid) {
+        shared_b = int32_t(min(gb_next, a.bits));
+        gb_next = __ldcg(a.gbound + q);
+      }
+      wait_k(tfull + b, bph, 0);
+      tc_fence_after();
+      {
+        int32_t v[kEpiCols];
+        if (((a.experiment & 1) && (g & 1)) || (a.experiment & 8)) {
+#pragma unroll
+          for (int j = 0; j < kEpiCols; ++j) v[j] = 1000;
+        } else {
+          tmem_ld32(taddr0 + b * kTcN, v);
+        }
+        tc_fence_before();  // accumulator drained into registers: hand it back
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + b);
+        const uint64_t id0 = lo + uint64_t(t) * kTcN + g * kEpiCols;
+        if constexpr (kDump) {
+          if (qvalid)
+            for (int j = 0; j < kEpiCols; ++j)
+              if (id0 + j < hi) a.dump[q * a.n + id0 + j] = v[j] + pq;
+        }
+        const int32_t thr = min(own, shared_b) - pq;
+        // tree minimum (independent 3-input mins, short dependency chain)
+        int32_t m8[11];
+#pragma unroll
+        for (int i = 0; i < 10; ++i) m8[i] = min(min(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+        m8[10] = min(v[30], v[31]);
+        const int32_t m3a = min(min(m8[0], m8[1]), m8[2]), m3b = min(min(m8[3], m8[4]), m8[5]);
+        const int32_t m3c = min(min(m8[6], m8[7]), m8[8]), m3d = min(m8[9], m8[10]);
+        const int32_t mn = min(min(m3a, m3b), min(m3c, m3d));
+        if (mn <= thr) {
+          // hit mask, then the (few) hits re-derive their distance from the code words (L2-hot)
+          uint32_t m = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) m |= uint32_t(v[j] <= thr) << j;
+          while (m) {
+            const uint32_t j = __ffs(m) - 1;
+            m &= m - 1;
+            const uint64_t id = id0 + j;
+            if (id >= hi) break;
+            uint32_t d = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) d += __popcll(__ldg(qp + w) ^ __ldg(a.codes + id * W + w));
+            list[cnt++] = (uint64_t(d) << 32) | uint32_t(id);
+          }
+        }
+        // warp-cooperative compaction of every list that reached 2k entries (scanlist.cuh)
+        uint32_t need = __ballot_sync(~0u, cnt >= 2 * a.k);
+        while (need) {
+          const int src = __ffs(need) - 1;
+          need &= need - 1;
+          uint64_t* l2 = reinterpret_cast<uint64_t*>(__shfl_sync(~0u, reinterpret_cast<uintptr_t>(list), src));
+          uint32_t c2 = __shfl_sync(~0u, cnt, src);
+          __syncwarp();
+          const uint32_t nt = compact_list(l2, c2, a.bits, a.k, hist);
+          if (lane == uint32_t(src)) {
+            cnt = c2;
+            own = int32_t(nt) - 1;
+            atomicMin(a.gbound + q, nt);
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (qvalid) a.counts[q * a.slots + slot] = cnt;
+  }
+  if (a.prof && lane == 0) {
+    unsigned long long* pr = a.prof + warp * 8;
+    atomicAdd(pr + 0, clock64() - t_start);
+    for (int i = 0; i < 4; ++i) atomicAdd(pr + 1 + i, wcyc[i]);
+    atomicAdd(pr + 5, (unsigned long long)T);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int KB>
+size_t tc_smem_bytes(uint32_t bits) {
+  using Cfg = TcCfg<KB>;
+  return Cfg::kSmem + (2 * Cfg::kStages + 2 * kAcc + 2 * kRaw) * 8 + 16 + size_t(kEpiWarps) * (bits + 1) * 4;
+}
+
+template <int KB>
+void launch_tc(const TcArgs& a, uint32_t grid, cudaStream_t st) {
+  const size_t smem = tc_smem_bytes<KB>(a.bits);
+  if (a.dump) {
+    MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    tc_scan_kernel<KB, true><<<grid, kTcThreads, smem, st>>>(a);
+  } else {
+    MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    tc_scan_kernel<KB, false><<<grid, kTcThreads, smem, st>>>(a);
+  }
+  MIHG_LAUNCH();
+}
+
+}  // namespace
+
+bool tc_scan_supported(uint32_t bits) { return bits >= 1 && bits <= 256; }
+
+// K7: the exhaustive k-NN of scan_knn_device on the tensor cores (same results bit for bit).
+void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                        const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                        uint32_t* d_dists, cudaStream_t st, int32_t* d_dump) {
+  if (k > n) throw InvalidArgument("scan_knn: k exceeds database size");
+  if (!tc_scan_supported(bits)) throw InvalidArgument("tc_scan: code width must be 1..256 bits");
+  if (nq == 0 || k == 0) return;
+  const uint32_t W = words_per_code(bits);
+  const uint32_t L = 2 * k + kEpiCols;
+  const uint64_t sms = uint64_t(device_sm_count());
+  for (uint64_t q0 = 0; q0 < nq;) {
+    uint64_t qn = nq - q0;
+    uint64_t qtiles = (qn + kTcM - 1) / kTcM;
+    // chunks: ~8 waves of one-CTA-per-SM work, each chunk at least 16 tiles of 256 codes
+    uint64_t nch = std::max<uint64_t>(1, (sms * 8 + qtiles - 1) / qtiles);
+    nch = std::min<uint64_t>(nch, std::max<uint64_t>(1, n / (16 * kTcN)));
+    nch = std::min<uint64_t>(nch, 1024 / kEpiGroups);  // gather_lists_kernel: <= 1024 slots
+    // list memory bound (~2 GiB): fewer queries per pass when k is large
+    const uint64_t per_q = kEpiGroups * nch * uint64_t(L) * 8 * 2;
+    const uint64_t qmax = std::max<uint64_t>(kTcM, (uint64_t(2) << 30) / per_q / kTcM * kTcM);
+    if (qn > qmax) {
+      qn = qmax;
+      qtiles = qn / kTcM;
+    }
+    if (d_dump) nch = 1, qn = nq, qtiles = (qn + kTcM - 1) / kTcM;
+    const uint64_t chunk = ((n + nch - 1) / nch + kTcN - 1) / kTcN * kTcN;
+    nch = (n + chunk - 1) / chunk;
+    TcArgs a{};
+    a.codes = d_codes;
+    a.n = n;
+    a.bits = bits;
+    a.k = k;
+    a.queries = d_queries + q0 * W;
+    a.nq = qn;
+    a.qtiles = uint32_t(qtiles);
+    a.chunk = chunk;
+    a.L = L;
+    a.slots = uint32_t(kEpiGroups * nch);
+    a.dump = d_dump;
+    if (const char* e = std::getenv("MIHG_TC_DESC_SWAP")) a.desc_swap = e[0] == '1';
+    if (const char* e = std::getenv("MIHG_TC_EXPERIMENT")) a.experiment = uint32_t(std::atoi(e));
+    const char* pe = std::getenv("MIHG_TC_PROF");
+    DeviceBuffer<unsigned long long> profbuf(pe && pe[0] == '1' ? 16 * 8 : 1, st);
+    if (pe && pe[0] == '1') {
+      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, 16 * 8 * 8, st));
+      a.prof = profbuf.get();
+    }
+    DeviceBuffer<uint64_t> lists(qn * a.slots * L, st), gathered(qn * a.slots * L, st);
+    DeviceBuffer<uint32_t> counts(qn * a.slots, st), gcount(qn, st), gbound(qn, st);
+    MIHG_CUDA(cudaMemsetAsync(gbound.get(), 0xFF, qn * 4, st));
+    a.gbound = gbound.get();
+    a.lists = lists.get();
+    a.counts = counts.get();
+    const uint32_t grid = uint32_t(qtiles * nch);
+    // live kernel timing for the bench's roofline (mihg_profile), on the launching stream
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    const bool prof = profile().enabled;
+    if (prof) {
+      if (!ev[0]) {
+        MIHG_CUDA(cudaEventCreate(&ev[0]));
+        MIHG_CUDA(cudaEventCreate(&ev[1]));
+      }
+      MIHG_CUDA(cudaEventRecord(ev[0], st));
+    }
+    switch (W) {
+      case 1: launch_tc<64>(a, grid, st); break;
+      case 2: launch_tc<128>(a, grid, st); break;
+      case 3: launch_tc<192>(a, grid, st); break;
+      default: launch_tc<256>(a, grid, st); break;
+    }
+    if (prof) MIHG_CUDA(cudaEventRecord(ev[1], st));
+    if (a.prof) {
+      unsigned long long h[16 * 8];
+      MIHG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+      MIHG_CUDA(cudaStreamSynchronize(st));
+      for (int w = 0; w < kLoadWarp + 1; ++w)
+        fprintf(stderr, "tcprof warp %2d: tiles %llu  cyc/tile total %.0f  wait0 %.0f  wait1 %.0f\n", w,
+                h[w * 8 + 5], double(h[w * 8]) / double(h[w * 8 + 5] ? h[w * 8 + 5] : 1),
+                double(h[w * 8 + 1]) / double(h[w * 8 + 5] ? h[w * 8 + 5] : 1),
+                double(h[w * 8 + 2]) / double(h[w * 8 + 5] ? h[w * 8 + 5] : 1));
+    }
+    gather_lists_kernel<<<unsigned(qn), 256, 0, st>>>(lists.get(), counts.get(), a.slots, L, gathered.get(),
+                                                      gcount.get());
+    MIHG_LAUNCH();
+    SelectArgs sa;
+    sa.keys = gathered.get();
+    sa.seg_stride = uint64_t(a.slots) * L;
+    sa.seg_count = gcount.get();
+    sa.k = k;
+    sa.id_base = id_base;
+    sa.out_ids = d_ids + q0 * k;
+    sa.out_dists = d_dists + q0 * k;
+    select_topk(sa, uint32_t(qn), st);
+    if (prof) {
+      float ms = 0;
+      MIHG_CUDA(cudaEventSynchronize(ev[1]));
+      MIHG_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      profile().scan_ms += ms;
+      profile().scan_launches += 1;
+    }
+    q0 += qn;
+  }
+}
+
+}  // namespace mihg

@@ -1,0 +1,84 @@
+"""GPU: the tensor-core exhaustive scan (K7, csrc/tcscan.cu) — every distance equals the
+reference's hamming_words (codes.hpp:38-42), and its top-k equals scan_knn (scan.hpp:43-68) through
+the oracle and through the POPC-pipe scan (K6) on the same inputs, ties included."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _popc_dist(q, x):
+    """[nq, n] Hamming distances of packed u64 rows (numpy restatement of hamming_words)."""
+    d = np.zeros((q.shape[0], x.shape[0]), np.int64)
+    for w in range(q.shape[1]):
+        v = np.bitwise_xor(q[:, w][:, None], x[:, w][None, :])
+        d += np.unpackbits(v.view(np.uint8).reshape(v.shape + (8,)), axis=-1).sum(-1).astype(np.int64)
+    return d
+
+
+@pytest.mark.parametrize("bits,n,nq", [(64, 3000, 200), (128, 2500, 130), (192, 1000, 70),
+                                       (256, 1300, 129), (70, 777, 5), (17, 600, 40)])
+def test_tc_distances_exact(cuda_ok, bits, n, nq):
+    import torch
+
+    from paper_1307_2982_b200 import _lib
+    import paper_1307_2982_b200 as mg
+
+    L = _lib.lib()
+    db = mg.gen_uniform(n, bits, 100 + bits).raw_words()
+    qs = mg.gen_uniform(nq, bits, 200 + bits).raw_words()
+    dd = torch.from_numpy(db.view(np.int64)).cuda()
+    dq = torch.from_numpy(qs.view(np.int64)).cuda()
+    out = torch.full((nq, n), -7, dtype=torch.int32, device="cuda")
+    _lib.check(L.mihg_tc_distances_device(C.c_void_p(dd.data_ptr()), n, bits, C.c_void_p(dq.data_ptr()), nq,
+                                          C.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    want = _popc_dist(qs, db)
+    got = out.cpu().numpy()
+    assert np.array_equal(got, want), f"bits={bits}: {np.argwhere(got != want)[:5]}"
+
+
+def _scan(idx, qs, k, kernel):
+    os.environ["MIHG_SCAN_KERNEL"] = kernel
+    try:
+        return idx.scan_knn_batch(qs, k)
+    finally:
+        os.environ.pop("MIHG_SCAN_KERNEL", None)
+
+
+@pytest.mark.parametrize("bits,n,nq,k", [(64, 50000, 300, 10), (64, 200000, 1000, 100), (128, 60000, 257, 33),
+                                         (256, 40000, 140, 100), (192, 30000, 64, 1), (40, 30000, 50, 500)])
+def test_tc_scan_matches_oracle_and_popc(cuda_ok, port, bits, n, nq, k):
+    import paper_1307_2982_b200 as mg
+
+    db = mg.gen_uniform(n, bits, 7 + bits)
+    qs = mg.gen_uniform(nq, bits, 8 + bits).raw_words()
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(bits, max(1, -(-bits // 32))), device=0)
+    ti, td = _scan(idx, qs, k, "tc")
+    pi, pd = _scan(idx, qs, k, "popc")
+    assert np.array_equal(ti, pi) and np.array_equal(td, pd)
+    if n * nq <= 2e7:
+        oi, od = port.scan_knn(db.raw_words(), bits, qs, k)
+        assert np.array_equal(ti, oi) and np.array_equal(td, od)
+
+
+def test_tc_scan_heavy_ties(cuda_ok):
+    """Few distinct codes: thousands of exact ties at every distance; the smaller id must win."""
+    import paper_1307_2982_b200 as mg
+
+    rng = np.random.default_rng(5)
+    centres = rng.integers(0, 2**63, size=(6, 2), dtype=np.int64).view(np.uint64)
+    pick = rng.integers(0, 6, size=70000)
+    codes = centres[pick].copy()
+    flip = rng.random(70000) < 0.1
+    codes[flip, 0] ^= np.uint64(1) << rng.integers(0, 64, size=flip.sum()).astype(np.uint64)
+    db = mg.CodeDatabase(128, codes)
+    qs = np.concatenate([centres, codes[:60]])
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(128, 4), device=0)
+    for k in (1, 100, 3000):
+        ti, td = _scan(idx, qs, k, "tc")
+        pi, pd = _scan(idx, qs, k, "popc")
+        assert np.array_equal(ti, pi) and np.array_equal(td, pd), k

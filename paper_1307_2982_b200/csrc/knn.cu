@@ -884,9 +884,9 @@ double scan_cost_per_code(uint32_t bits) {
   const uint32_t W = words_per_code(bits);
   if (scan_kernel_for(bits) != ScanKernel::Tensor) return W;
   const char* e = std::getenv("MIHG_TC_SPEEDUP");
-  // measured pair rates (tools/bench_tcscan.py, n = 1e8, 1e4 queries): K7 ~3.3e12 pairs/s at every
-  // width (accumulator-drain bound); K6 1.95e12 (W=1) ... 5.3e11 (W=4) pairs/s
-  const double f = e ? std::atof(e) : (W == 1 ? 1.7 : W == 2 ? 3.0 : W == 3 ? 4.5 : 6.0);
+  // measured pair rates on B200 (bench.py --method scan, 1e4 queries): K7 4.2e12 pairs/s (64-bit,
+  // n = 1e8) ... 2.9e12 (256-bit, n = 1e9); K6 1.95e12 (W=1) ... 5.3e11 (W=4) pairs/s
+  const double f = e ? std::atof(e) : (W == 1 ? 2.1 : W == 2 ? 3.5 : W == 3 ? 4.5 : 5.5);
   return W / f;
 }
 

@@ -7,18 +7,18 @@
 // M=128 x N=256 x K=32 instruction evaluates 32768 (query, code) pairs on 32 bits; the POPC pipe
 // needs 2048 instructions for the same work.
 //
-// CTA = 128 queries (TMEM lanes) x one id chunk of the database, one CTA per SM, warp-specialised:
-//   warps 0-7   epilogue: thread (warp % 4, lane) owns query row 32 (warp % 4) + lane; group
-//               g = warp / 4 drains columns [64 g, 64 g + 64) of every 128-code tile and keeps its
+// Persistent CTAs (one per SM), each over a contiguous range of (128-query tile, id chunk) work
+// items; consecutive items of one query tile form a segment (one id range, one set of lists).
+// 22 warps, warp-specialised:
+//   warps 0-15  epilogue: thread (warp % 4, lane) owns query row 32 (warp % 4) + lane; group
+//               g = warp / 4 drains columns [32 g, 32 g + 32) of every 128-code tile and keeps its
 //               own candidate list per query (id order, compacted to the exact top-k when it reaches
 //               2k entries; scanlist.cuh, as in K6), under a bound shared by all lists of the query.
-//   warps 8-11  producers: each thread takes one code per tile from the raw ring and expands it
-//               to K bytes of 0/1 in the no-swizzle K-major canonical layout of the B operand
-//               (8-row x 16-byte core matrices).
-//   warp 12     TMEM allocation and the single-thread tcgen05.mma issue.
-//   warp 13     loader: one thread keeps kRaw raw code tiles in flight from HBM/L2 into shared
-//               memory with 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx) — the
-//               latency of the shared (L2-resident) chunk is far longer than a tile's MMA.
+//   warps 16-19 producers: each thread takes one code per tile from the raw ring and expands it
+//               to K bytes of 0/1 in the 128-byte-swizzled K-major layout of the B operand.
+//   warp 20     TMEM allocation and the single-thread tcgen05.mma issue.
+//   warp 21     loader: one thread keeps kRaw raw code tiles in flight from HBM/L2 into shared
+//               memory with 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx).
 // Pipelines: B stages full/empty (producers <-> MMA, mbarriers; tcgen05.commit frees a stage) and
 // four TMEM accumulators of 128 columns (MMA <-> epilogue), so the MMA runs up to four tiles
 // ahead of the accumulator drain.
@@ -38,7 +38,8 @@ namespace {
 
 constexpr int kTcM = 128;        // queries per CTA (TMEM lanes)
 constexpr int kTcN = 128;        // codes per tile (MMA N)
-constexpr int kAcc = 4;          // TMEM accumulators of kTcN columns (512 columns allocated)
+constexpr int kAcc = 3;          // TMEM accumulators of kTcN columns at [0, 384); A (queries) at 384
+constexpr uint32_t kATmemCol = kAcc * kTcN;
 constexpr int kEpiGroups = 4;    // epilogue groups of 4 warps; group g drains columns [32 g, 32 g + 32)
 constexpr int kEpiCols = kTcN / kEpiGroups;
 constexpr int kEpiWarps = 4 * kEpiGroups;
@@ -55,16 +56,19 @@ struct TcArgs {
   const uint64_t* queries;
   uint64_t nq;
   uint32_t qtiles;
-  uint64_t chunk;  // codes per chunk (multiple of kTcN)
+  uint32_t nch;      // id chunks per query tile; work item = (query tile, chunk), tile-major
+  uint64_t chunk;    // codes per chunk (multiple of kTcN)
+  uint32_t ipc;      // work items per CTA (a contiguous range)
+  uint32_t spq;      // CTAs touching one query tile, at most (list slots = spq * kEpiGroups)
   uint32_t L;
-  uint64_t* lists;   // [q][slot][L], slot = chunk * kEpiGroups + group
-  uint32_t* counts;  // [q][slot]
+  uint64_t* lists;   // [q][slot][L], slot = (CTA - first CTA of the tile) * kEpiGroups + group
+  uint32_t* counts;  // [q][slot], zero for unused slots
   uint32_t slots;
   int32_t* dump;     // debug: nq x n distances (tests only), or nullptr
   uint32_t* gbound;  // [q]: smallest k-th distance proven by any list of the query (0xFFFFFFFF = none)
-  unsigned long long* prof;  // debug (MIHG_TC_PROF=1): [warp][8] cycle counters summed over CTAs
-  uint32_t experiment;  // timing experiments only (MIHG_TC_EXPERIMENT): 1 = group 1 skips its TMEM load
-  uint32_t desc_swap;  // debug (MIHG_TC_DESC_SWAP=1): exchange LBO and SBO in the descriptors
+  unsigned long long* prof;  // debug (MIHG_TC_PROF=1): [32 warps][8] cycle counters summed over CTAs
+  uint32_t mma_only;         // timing probe (MIHG_TC_MMA_ONLY=1|2): only the MMA stream runs (2: rotating
+                             // B stages); results are NOT produced — measures the tensor ceiling
 };
 
 // ---- PTX wrappers (tcgen05 / mbarrier) ----
@@ -84,20 +88,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-// test_wait spin (no suspend): experiment 64
-__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(a), "r"(parity)
@@ -129,11 +119,32 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint6
       : "memory");
 }
 
-// Shared-memory matrix descriptor, K-major, no swizzle: core matrices of 8 rows x 16 bytes stored
-// contiguously; LBO = byte step between K-adjacent core matrices, SBO = between 8-row groups.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  return uint64_t((addr & 0x3FFFFu) >> 4) | (uint64_t(lbo >> 4) << 16) | (uint64_t(sbo >> 4) << 32) |
-         (uint64_t(1) << 46);  // version 1 (tcgen05), base offset 0, layout SWIZZLE_NONE
+// D[tmem] (+)= A[tmem] . B[smem]^T, kind::i8 (A signed in TMEM, B unsigned in shared memory)
+__device__ __forceinline__ void tc_mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 TMEM lanes x 16 consecutive 32-bit columns <- 16 registers per thread (lane = thread).
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+// Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 bytes in 1024-byte
+// atoms of 8 rows (SBO = 1024), the 16-byte chunk c of row r stored at c ^ (r mod 8); a K extent
+// above 128 bytes continues in the next 128-byte K block (a separate rows x 128 B region).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+  return uint64_t((addr & 0x3FFFFu) >> 4) | (uint64_t(16 >> 4) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);  // version 1, base offset 0, SWIZZLE_128B
 }
 
 // Instruction descriptor: kind::i8, D = s32, A = s8 (signed), B = u8, both K-major, M x N.
@@ -158,10 +169,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
 // 4 bits -> 4 bytes of 0/1 (bit i -> byte i)
 __device__ __forceinline__ uint32_t spread4(uint32_t x) { return (x * 0x00204081u) & 0x01010101u; }
 
-// byte offset of (row r, 16-byte K chunk c) in a no-swizzle K-major operand with KB bytes per row
+// byte offset of (row r, 16-byte K chunk c) in a 128B-swizzled K-major operand of `rows` rows
 template <int KB>
-__device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t c) {
-  return (r >> 3) * (KB * 8) + c * 128 + (r & 7) * 16;
+__device__ __forceinline__ uint32_t core_off(uint32_t r, uint32_t c, uint32_t rows) {
+  return (c >> 3) * (rows * 128) + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
+
+// start address of MMA k-step kk (32 bytes of K) in such an operand
+__device__ __forceinline__ uint32_t kstep_addr(uint32_t base, int kk, uint32_t rows) {
+  return base + (kk >> 2) * (rows * 128) + (kk & 3) * 32;
 }
 
 // The 16-byte-aligned part of a raw tile's code bytes (TMA bulk copies need 16-byte alignment and
@@ -180,11 +196,13 @@ __device__ __forceinline__ void raw_span(const uint64_t* codes, uint64_t id0, ui
 template <int KB>
 struct TcCfg {
   static constexpr int W = KB / 64;
-  static constexpr uint32_t kA = kTcM * KB;
-  static constexpr uint32_t kB = kTcN * KB;
-  static constexpr int kStages = KB <= 64 ? 8 : (KB <= 128 ? 6 : (KB <= 192 ? 4 : 3));
+  static constexpr uint32_t kKBp = (KB + 127) / 128 * 128;  // whole 128-byte swizzle rows
+  static constexpr uint32_t kA = 0;  // A lives in TMEM
+  static constexpr uint32_t kB = kTcN * kKBp;
+  static constexpr int kStages = KB <= 64 ? 8 : (KB <= 128 ? 6 : 4);
   static constexpr uint32_t kRawBytes = kTcN * W * 8;  // one raw tile of packed codes
   static constexpr uint32_t kSmem = 1024 + kA + kStages * kB + kRaw * kRawBytes;  // + barriers/hist
+  static_assert(kStages > kAcc, "the stage barriers double as accumulator-ready signals");
 };
 
 template <int KB, bool kDump>
@@ -194,8 +212,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = base;
-  uint8_t* sB = base + Cfg::kA;
+  uint8_t* sB = base;
   uint8_t* sRaw = sB + S * Cfg::kB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRaw + kRaw * Cfg::kRawBytes);
   uint64_t* full = bars;
@@ -208,21 +225,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   uint32_t* hist_all = tmem_slot + 4;  // kEpiWarps * (bits + 1)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool spin = (a.experiment & 64) != 0;
   unsigned long long wcyc[4] = {0, 0, 0, 0};
   auto wait_k = [&](uint64_t* bar, uint32_t parity, int kind) {
     const unsigned long long c0 = a.prof ? clock64() : 0;
-    if (spin) mbar_spin(bar, parity);
-    else mbar_wait(bar, parity);
+    mbar_wait(bar, parity);
     if (a.prof) wcyc[kind] += clock64() - c0;
   };
-  auto wait = [&](uint64_t* bar, uint32_t parity) { wait_k(bar, parity, 0); };
   const unsigned long long t_start = clock64();
-  const uint32_t qtile = blockIdx.x % a.qtiles, chunk = blockIdx.x / a.qtiles;
-  const uint64_t q0 = uint64_t(qtile) * kTcM;
-  const uint64_t lo = uint64_t(chunk) * a.chunk;
-  const uint64_t hi = min(a.n, lo + a.chunk);
-  const uint32_t T = uint32_t((hi - lo + kTcN - 1) / kTcN);
 
   if (warp == kMmaWarp) {
     if (lane == 0) {
@@ -244,156 +253,190 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // A operand: the 128 queries of the tile as +1 (bit 0) / -1 (bit 1) bytes; padding rows zero
-  for (uint32_t u = threadIdx.x; u < uint32_t(kTcM) * (KB / 16); u += kTcThreads) {
-    const uint32_t r = u / (KB / 16), c = u % (KB / 16);
-    const uint64_t q = q0 + r;
-    uint4 o = make_uint4(0, 0, 0, 0);
-    if (q < a.nq) {
-      const uint32_t h = uint32_t(__ldg(a.queries + q * W + (c >> 2)) >> ((c & 3) * 16)) & 0xFFFFu;
-      o.x = (spread4(h & 0xF) * 0xFEu) ^ 0x01010101u;
-      o.y = (spread4((h >> 4) & 0xF) * 0xFEu) ^ 0x01010101u;
-      o.z = (spread4((h >> 8) & 0xF) * 0xFEu) ^ 0x01010101u;
-      o.w = (spread4(h >> 12) * 0xFEu) ^ 0x01010101u;
-    }
-    *reinterpret_cast<uint4*>(sA + core_off<KB>(r, c)) = o;
-  }
-  fence_proxy_async();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == kMmaWarp) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
-      const uint32_t a_addr = smem_u32(sA), b_addr = smem_u32(sB);
-      for (uint32_t t = 0; t < T; ++t) {
-        const uint32_t s = t % S, ph = (t / S) & 1, b = t % kAcc, bph = (t / kAcc) & 1;
-        wait_k(tempty + b, bph ^ 1, 0);
-        wait_k(full + s, ph, 1);
-        tc_fence_after();
+  // This CTA's work items [i0, i1) (tile-major): consecutive items of one query tile form a
+  // segment over one contiguous id range, with one candidate list per (query, group).
+  const uint64_t items = uint64_t(a.qtiles) * a.nch;
+  const uint64_t i0 = uint64_t(blockIdx.x) * a.ipc, i1 = min(items, i0 + a.ipc);
+  uint32_t tg = 0;  // tiles processed by this CTA so far: drives every pipeline phase
+  uint32_t mo_phase = 0;  // mma_only probe
+  uint32_t tiles_total = 0;
+  for (uint64_t it = i0; it < i1;) {
+    const uint32_t Q = uint32_t(it / a.nch);
+    const uint64_t it_end = min(i1, uint64_t(Q + 1) * a.nch);
+    const uint64_t lo = (it - uint64_t(Q) * a.nch) * a.chunk;
+    const uint64_t hi = min(a.n, (it_end - uint64_t(Q) * a.nch) * a.chunk);
+    const uint32_t T = uint32_t((hi - lo + kTcN - 1) / kTcN);
+    const uint32_t slot0 = (blockIdx.x - uint32_t((uint64_t(Q) * a.nch) / a.ipc)) * kEpiGroups;
+    const uint64_t q0 = uint64_t(Q) * kTcM;
+    it = it_end;
+
+    // A operand in TMEM (columns kATmemCol..): lane r = query q0 + r as K bytes of +1 (bit 0) /
+    // -1 (bit 1), four per 32-bit column; padding rows zero. Written by warps 0-3 (lanes 32 w..).
+    if (warp < 4) {
+      const uint32_t r = warp * 32 + lane;
+      const uint64_t q = q0 + r;
 #pragma unroll
-        for (int kk = 0; kk < KB / 32; ++kk) {
-          const uint32_t lbo = a.desc_swap ? KB * 8 : 128, sbo = a.desc_swap ? 128 : KB * 8;
-          const uint64_t ad = smem_desc(a_addr + kk * 256, lbo, sbo);
-          const uint64_t bd = smem_desc(b_addr + s * Cfg::kB + kk * 256, lbo, sbo);
-          if (!(a.experiment & 2)) tc_mma_i8(tmem + b * kTcN, ad, bd, idesc, kk > 0);
+      for (int c16 = 0; c16 < KB / 64; ++c16) {  // 16 columns = 64 bytes = 64 query bits per store
+        uint32_t w16[16];
+        const uint64_t word = q < a.nq ? __ldg(a.queries + q * W + c16) : 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t nib = uint32_t(word >> (4 * i)) & 0xFu;
+          w16[i] = q < a.nq ? ((spread4(nib) * 0xFEu) ^ 0x01010101u) : 0u;
         }
-        tc_commit(empty + s);
-        tc_commit(tfull + b);
+        tmem_st16(tmem + ((warp * 32) << 16) + kATmemCol + c16 * 16, w16);
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    __syncwarp();
-  } else if (warp == kLoadWarp) {
-    // ===== loader: raw code tiles -> shared memory (TMA bulk copies) =====
-    if (lane == 0) {
-      for (uint32_t t = 0; t < T; ++t) {
-        const uint32_t r = t % kRaw;
-        wait(rempty + r, ((t / kRaw) & 1) ^ 1);
-        uint32_t skip, bytes;
-        raw_span<W>(a.codes, lo + uint64_t(t) * kTcN, hi, skip, bytes);
-        const uint32_t bar = smem_u32(rfull + r);
-        if (bytes) {
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(sRaw + r * Cfg::kRawBytes)),
-              "l"(reinterpret_cast<const uint8_t*>(a.codes + (lo + uint64_t(t) * kTcN) * W) + skip), "r"(bytes),
-              "r"(bar)
-              : "memory");
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (a.mma_only) {
+      if (warp == kMmaWarp && lane == 0) {
+        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
+        const uint32_t b_addr = smem_u32(sB);
+        for (uint32_t t = tg; t < tg + T; ++t) {
+#pragma unroll
+          for (int kk = 0; kk < KB / 32; ++kk)
+            tc_mma_i8_ts(tmem + (t % kAcc) * kTcN, tmem + kATmemCol + kk * 8,
+                         smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kTcN)),
+                         idesc, kk > 0);
+        }
+        tc_commit(tfull);
+        mbar_wait(tfull, mo_phase);  // drains this segment's MMAs
+        mo_phase ^= 1;
+      }
+      __syncwarp();
+    } else if (warp == kMmaWarp) {
+      // ===== MMA issuer =====
+      if (lane == 0) {
+        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
+        const uint32_t b_addr = smem_u32(sB);
+        for (uint32_t t = tg; t < tg + T; ++t) {
+          const uint32_t s = t % S, ph = (t / S) & 1, b = t % kAcc, bph = (t / kAcc) & 1;
+          wait_k(tempty + b, bph ^ 1, 0);
+          wait_k(full + s, ph, 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < KB / 32; ++kk) {  // K = 32 bytes = 8 TMEM columns of A per step
+            const uint64_t bd = smem_desc_sw128(kstep_addr(b_addr + s * Cfg::kB, kk, kTcN));
+            tc_mma_i8_ts(tmem + b * kTcN, tmem + kATmemCol + kk * 8, bd, idesc, kk > 0);
+          }
+          tc_commit(empty + s);  // ONE commit per tile: frees the B stage and publishes the accumulator
+        }
+      }
+      __syncwarp();
+    } else if (warp == kLoadWarp) {
+      // ===== loader: raw code tiles -> shared memory (TMA bulk copies) =====
+      if (lane == 0) {
+        for (uint32_t t = tg; t < tg + T; ++t) {
+          const uint32_t r = t % kRaw;
+          wait_k(rempty + r, ((t / kRaw) & 1) ^ 1, 0);
+          const uint64_t id0 = lo + uint64_t(t - tg) * kTcN;
+          uint32_t skip, bytes;
+          raw_span<W>(a.codes, id0, hi, skip, bytes);
+          const uint32_t bar = smem_u32(rfull + r);
+          if (bytes) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sRaw + r * Cfg::kRawBytes)),
+                "l"(reinterpret_cast<const uint8_t*>(a.codes + id0 * W) + skip), "r"(bytes), "r"(bar)
+                : "memory");
+          } else {
+            mbar_arrive(rfull + r);
+          }
+        }
+      }
+      __syncwarp();
+    } else if (warp >= kEpiWarps) {
+      // ===== producers: raw code -> 0/1 bytes =====
+      const uint32_t p = threadIdx.x - kEpiWarps * 32;  // code row within the tile
+      for (uint32_t t = tg; t < tg + T; ++t) {
+        const uint32_t s = t % S, ph = (t / S) & 1, r = t % kRaw;
+        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN, id = id0 + p;
+        uint32_t skip, tbytes;
+        raw_span<W>(a.codes, id0, hi, skip, tbytes);
+        wait_k(rfull + r, (t / kRaw) & 1, 0);
+        uint64_t cur[W];
+        if (p * W * 8 >= skip && (p + 1) * W * 8 <= skip + tbytes) {
+          const uint64_t* src = reinterpret_cast<const uint64_t*>(sRaw + r * Cfg::kRawBytes + p * W * 8 - skip);
+#pragma unroll
+          for (int w = 0; w < W; ++w) cur[w] = src[w];
+        } else if (id < hi) {  // misaligned head / odd tail of the tile
+#pragma unroll
+          for (int w = 0; w < W; ++w) cur[w] = __ldg(a.codes + id * W + w);
         } else {
-          mbar_arrive(rfull + r);
+#pragma unroll
+          for (int w = 0; w < W; ++w) cur[w] = 0;
         }
-      }
-    }
-    __syncwarp();
-  } else if (warp >= kEpiWarps) {
-    // ===== producers: raw code -> 0/1 bytes =====
-    const uint32_t p = threadIdx.x - kEpiWarps * 32;  // code row within the tile
-    for (uint32_t t = 0; t < T; ++t) {
-      const uint32_t s = t % S, ph = (t / S) & 1, r = t % kRaw;
-      const uint64_t id = lo + uint64_t(t) * kTcN + p;
-      uint32_t skip, tbytes;
-      raw_span<W>(a.codes, lo + uint64_t(t) * kTcN, hi, skip, tbytes);
-      wait_k(rfull + r, (t / kRaw) & 1, 0);
-      uint64_t cur[W];
-      if (p * W * 8 >= skip && (p + 1) * W * 8 <= skip + tbytes) {
-        const uint64_t* src = reinterpret_cast<const uint64_t*>(sRaw + r * Cfg::kRawBytes + p * W * 8 - skip);
-#pragma unroll
-        for (int w = 0; w < W; ++w) cur[w] = src[w];
-      } else if (id < hi) {  // tail of the last tile (not a multiple of 16 bytes)
-#pragma unroll
-        for (int w = 0; w < W; ++w) cur[w] = __ldg(a.codes + id * W + w);
-      } else {
-#pragma unroll
-        for (int w = 0; w < W; ++w) cur[w] = 0;
-      }
-      if (a.experiment & 16) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) cur[w] = 0;
-      }
-      wait_k(empty + s, ph ^ 1, 1);
-      uint8_t* dst = sB + s * Cfg::kB;
-      if (!(a.experiment & 4))
+        wait_k(empty + s, ph ^ 1, 1);
+        const unsigned long long c_x = a.prof ? clock64() : 0;
+        uint8_t* dst = sB + s * Cfg::kB;
 #pragma unroll
         for (int c = 0; c < KB / 16; ++c) {
           const uint32_t h = uint32_t(cur[c >> 2] >> ((c & 3) * 16)) & 0xFFFFu;
           const uint4 o = make_uint4(spread4(h & 0xF), spread4((h >> 4) & 0xF), spread4((h >> 8) & 0xF),
                                      spread4(h >> 12));
-          *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c)) = o;
+          *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c, kTcN)) = o;
         }
-      if (!(a.experiment & 32)) fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(full + s);
-        mbar_arrive(rempty + r);  // the raw words were consumed by the expansion above
+        const unsigned long long c_f = a.prof ? clock64() : 0;
+        fence_proxy_async();
+        __syncwarp();
+        if (a.prof) {
+          wcyc[2] += clock64() - c_f;
+          wcyc[3] += c_f - c_x;
+        }
+        if (lane == 0) {
+          mbar_arrive(full + s);
+          mbar_arrive(rempty + r);  // the raw words were consumed by the expansion above
+        }
       }
-    }
-  } else {
-    // ===== epilogue: TMEM -> registers -> bound test -> candidate list =====
-    // Accept bound per query: min(own, shared). own = bits until the list is first compacted, then
-    // (its k-th distance) - 1: a later id at that distance ranks below all k kept entries.
-    // shared = gbound[q], the smallest k-th distance any list of this query has proven (atomicMin
-    // after each compaction); ties at it are still accepted (another slot may hold smaller ids).
-    const uint32_t g = warp >> 2, quad = warp & 3;
-    const uint32_t row = quad * 32 + lane;
-    const uint64_t q = q0 + row;
-    const bool qvalid = q < a.nq;
-    const uint64_t* qp = a.queries + (qvalid ? q : 0) * W;
-    int32_t pq = 0;
-    if (qvalid)
-      for (int w = 0; w < W; ++w) pq += __popcll(__ldg(qp + w));
-    int32_t own = qvalid ? int32_t(a.bits) : -1;
-    uint32_t cnt = 0;
-    const uint32_t slot = chunk * kEpiGroups + g;
-    uint64_t* list = a.lists + ((qvalid ? q : 0) * a.slots + slot) * uint64_t(a.L);
-    uint32_t* hist = hist_all + warp * (a.bits + 1);
-    const uint32_t taddr0 = tmem + ((quad * 32) << 16) + g * kEpiCols;
-    // the shared bound is refreshed every 4 tiles from a load issued 4 tiles earlier (L2 latency)
-    uint32_t gb_next = qvalid ? __ldcg(a.gbound + q) : 0u;
-    int32_t shared_b = qvalid ? int32_t(a.bits) : -1;
-    for (uint32_t t = 0; t < T; ++t) {
-      const uint32_t b = t % kAcc, bph = (t / kAcc) & 1;
-      if ((t & 3) == 0 && qvalid) {
-        shared_b = int32_t(min(gb_next, a.bits));
-        gb_next = __ldcg(a.gbound + q);
-      }
-      wait_k(tfull + b, bph, 0);
-      tc_fence_after();
-      {
+    } else {
+      // ===== epilogue: TMEM -> registers -> bound test -> candidate list =====
+      // Accept bound per query: min(own, shared). own = bits until the list is first compacted,
+      // then (its k-th distance) - 1: a later id at that distance ranks below all k kept entries.
+      // shared = gbound[q], the smallest k-th distance any list of this query has proven
+      // (atomicMin after each compaction); ties at it are still accepted (another slot may hold
+      // smaller ids).
+      const uint32_t g = warp >> 2, quad = warp & 3;
+      const uint32_t row = quad * 32 + lane;
+      const uint64_t q = q0 + row;
+      const bool qvalid = q < a.nq;
+      const uint64_t* qp = a.queries + (qvalid ? q : 0) * W;
+      int32_t pq = 0;
+      if (qvalid)
+        for (int w = 0; w < W; ++w) pq += __popcll(__ldg(qp + w));
+      int32_t own = qvalid ? int32_t(a.bits) : -1;
+      uint32_t cnt = 0;
+      const uint32_t slot = slot0 + g;
+      uint64_t* list = a.lists + ((qvalid ? q : 0) * a.slots + slot) * uint64_t(a.L);
+      uint32_t* hist = hist_all + warp * (a.bits + 1);
+      const uint32_t taddr0 = tmem + ((quad * 32) << 16) + g * kEpiCols;
+      // the shared bound is refreshed every 4 tiles from a load issued 4 tiles earlier (L2 latency)
+      uint32_t gb_next = qvalid ? __ldcg(a.gbound + q) : 0u;
+      int32_t shared_b = qvalid ? int32_t(a.bits) : -1;
+      for (uint32_t t = tg; t < tg + T; ++t) {
+        const uint32_t b = t % kAcc, bph = (t / kAcc) & 1;
+        if (((t - tg) & 3) == 0 && qvalid) {
+          shared_b = int32_t(min(gb_next, a.bits));
+          gb_next = __ldcg(a.gbound + q);
+        }
+        wait_k(empty + (t % S), (t / S) & 1, 0);  // the tile's MMAs are complete (S > kAcc: no aliasing)
+        tc_fence_after();
         int32_t v[kEpiCols];
-        if (((a.experiment & 1) && (g & 1)) || (a.experiment & 8)) {
-#pragma unroll
-          for (int j = 0; j < kEpiCols; ++j) v[j] = 1000;
-        } else {
-          tmem_ld32(taddr0 + b * kTcN, v);
-        }
+        tmem_ld32(taddr0 + b * kTcN, v);
         tc_fence_before();  // accumulator drained into registers: hand it back
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + b);
-        const uint64_t id0 = lo + uint64_t(t) * kTcN + g * kEpiCols;
+        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols;
         if constexpr (kDump) {
           if (qvalid)
             for (int j = 0; j < kEpiCols; ++j)
@@ -441,17 +484,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           __syncwarp();
         }
       }
+      if (qvalid) a.counts[q * a.slots + slot] = cnt;
     }
-    if (qvalid) a.counts[q * a.slots + slot] = cnt;
+    tg += T;
+    tiles_total += T;
+    // segment end: every MMA of the segment was drained by the epilogue, so A may be reloaded
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
   }
   if (a.prof && lane == 0) {
     unsigned long long* pr = a.prof + warp * 8;
     atomicAdd(pr + 0, clock64() - t_start);
     for (int i = 0; i < 4; ++i) atomicAdd(pr + 1 + i, wcyc[i]);
-    atomicAdd(pr + 5, (unsigned long long)T);
+    atomicAdd(pr + 5, (unsigned long long)tiles_total);
   }
-  tc_fence_before();
-  __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -464,17 +511,18 @@ size_t tc_smem_bytes(uint32_t bits) {
   return Cfg::kSmem + (2 * Cfg::kStages + 2 * kAcc + 2 * kRaw) * 8 + 16 + size_t(kEpiWarps) * (bits + 1) * 4;
 }
 
+template <int KB, bool kDump>
+void launch_tc_k(const TcArgs& a, uint32_t grid, cudaStream_t st) {
+  const size_t smem = tc_smem_bytes<KB>(a.bits);
+  MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, kDump>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  tc_scan_kernel<KB, kDump><<<grid, kTcThreads, smem, st>>>(a);
+  MIHG_LAUNCH();
+}
+
 template <int KB>
 void launch_tc(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  const size_t smem = tc_smem_bytes<KB>(a.bits);
-  if (a.dump) {
-    MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    tc_scan_kernel<KB, true><<<grid, kTcThreads, smem, st>>>(a);
-  } else {
-    MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    tc_scan_kernel<KB, false><<<grid, kTcThreads, smem, st>>>(a);
-  }
-  MIHG_LAUNCH();
+  if (a.dump) launch_tc_k<KB, true>(a, grid, st);
+  else launch_tc_k<KB, false>(a, grid, st);
 }
 
 }  // namespace
@@ -494,20 +542,35 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
   for (uint64_t q0 = 0; q0 < nq;) {
     uint64_t qn = nq - q0;
     uint64_t qtiles = (qn + kTcM - 1) / kTcM;
-    // chunks: ~8 waves of one-CTA-per-SM work, each chunk at least 16 tiles of 256 codes
-    uint64_t nch = std::max<uint64_t>(1, (sms * 8 + qtiles - 1) / qtiles);
+    // Persistent CTAs, one per SM, each over a contiguous range of (query tile, chunk) items.
+    // nch is a multiple of sms / gcd(qtiles, sms) so the items divide evenly over the SMs, with
+    // at least 8 items per CTA; chunks of at least 16 tiles.
+    uint64_t g = sms, r = qtiles;
+    while (r) { const uint64_t t = g % r; g = r; r = t; }
+    const uint64_t step = sms / g;
+    uint64_t nch = step;
+    while (nch * qtiles < 8 * sms) nch += step;
     nch = std::min<uint64_t>(nch, std::max<uint64_t>(1, n / (16 * kTcN)));
-    nch = std::min<uint64_t>(nch, 1024 / kEpiGroups);  // gather_lists_kernel: <= 1024 slots
+    uint64_t chunk = ((n + nch - 1) / nch + kTcN - 1) / kTcN * kTcN;
+    nch = (n + chunk - 1) / chunk;
+    uint64_t items = qtiles * nch, ipc = (items + sms - 1) / sms;
+    auto spq_of = [&](uint64_t qt, uint64_t nchv, uint64_t ipcv) {
+      uint64_t m = 1;
+      for (uint64_t Q = 0; Q < qt; ++Q) m = std::max(m, ((Q + 1) * nchv - 1) / ipcv - (Q * nchv) / ipcv + 1);
+      return m;
+    };
+    uint64_t spq = spq_of(qtiles, nch, ipc);
     // list memory bound (~2 GiB): fewer queries per pass when k is large
-    const uint64_t per_q = kEpiGroups * nch * uint64_t(L) * 8 * 2;
+    const uint64_t per_q = kEpiGroups * spq * uint64_t(L) * 8 * 2;
     const uint64_t qmax = std::max<uint64_t>(kTcM, (uint64_t(2) << 30) / per_q / kTcM * kTcM);
     if (qn > qmax) {
       qn = qmax;
       qtiles = qn / kTcM;
+      items = qtiles * nch;
+      ipc = (items + sms - 1) / sms;
+      spq = spq_of(qtiles, nch, ipc);
     }
-    if (d_dump) nch = 1, qn = nq, qtiles = (qn + kTcM - 1) / kTcM;
-    const uint64_t chunk = ((n + nch - 1) / nch + kTcN - 1) / kTcN * kTcN;
-    nch = (n + chunk - 1) / chunk;
+    const uint32_t grid = uint32_t((items + ipc - 1) / ipc);
     TcArgs a{};
     a.codes = d_codes;
     a.n = n;
@@ -516,25 +579,28 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     a.queries = d_queries + q0 * W;
     a.nq = qn;
     a.qtiles = uint32_t(qtiles);
+    a.nch = uint32_t(nch);
     a.chunk = chunk;
+    a.ipc = uint32_t(ipc);
+    a.spq = uint32_t(spq);
     a.L = L;
-    a.slots = uint32_t(kEpiGroups * nch);
+    a.slots = uint32_t(kEpiGroups * spq);
     a.dump = d_dump;
-    if (const char* e = std::getenv("MIHG_TC_DESC_SWAP")) a.desc_swap = e[0] == '1';
-    if (const char* e = std::getenv("MIHG_TC_EXPERIMENT")) a.experiment = uint32_t(std::atoi(e));
+    if (const char* mo = std::getenv("MIHG_TC_MMA_ONLY")) a.mma_only = uint32_t(std::atoi(mo));
     const char* pe = std::getenv("MIHG_TC_PROF");
-    DeviceBuffer<unsigned long long> profbuf(pe && pe[0] == '1' ? 16 * 8 : 1, st);
-    if (pe && pe[0] == '1') {
-      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, 16 * 8 * 8, st));
+    const bool dbg_prof = pe && pe[0] == '1';
+    DeviceBuffer<unsigned long long> profbuf(dbg_prof ? 32 * 8 : 1, st);
+    if (dbg_prof) {
+      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, 32 * 8 * 8, st));
       a.prof = profbuf.get();
     }
     DeviceBuffer<uint64_t> lists(qn * a.slots * L, st), gathered(qn * a.slots * L, st);
     DeviceBuffer<uint32_t> counts(qn * a.slots, st), gcount(qn, st), gbound(qn, st);
+    MIHG_CUDA(cudaMemsetAsync(counts.get(), 0, qn * a.slots * 4, st));
     MIHG_CUDA(cudaMemsetAsync(gbound.get(), 0xFF, qn * 4, st));
     a.gbound = gbound.get();
     a.lists = lists.get();
     a.counts = counts.get();
-    const uint32_t grid = uint32_t(qtiles * nch);
     // live kernel timing for the bench's roofline (mihg_profile), on the launching stream
     static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
     const bool prof = profile().enabled;
@@ -552,15 +618,16 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
       default: launch_tc<256>(a, grid, st); break;
     }
     if (prof) MIHG_CUDA(cudaEventRecord(ev[1], st));
-    if (a.prof) {
-      unsigned long long h[16 * 8];
+    if (dbg_prof) {
+      unsigned long long h[32 * 8];
       MIHG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
       MIHG_CUDA(cudaStreamSynchronize(st));
-      for (int w = 0; w < kLoadWarp + 1; ++w)
-        fprintf(stderr, "tcprof warp %2d: tiles %llu  cyc/tile total %.0f  wait0 %.0f  wait1 %.0f\n", w,
-                h[w * 8 + 5], double(h[w * 8]) / double(h[w * 8 + 5] ? h[w * 8 + 5] : 1),
-                double(h[w * 8 + 1]) / double(h[w * 8 + 5] ? h[w * 8 + 5] : 1),
-                double(h[w * 8 + 2]) / double(h[w * 8 + 5] ? h[w * 8 + 5] : 1));
+      for (int w = 0; w <= kLoadWarp; ++w) {
+        const double tl = double(h[w * 8 + 5] ? h[w * 8 + 5] : 1);
+        fprintf(stderr, "tcprof warp %2d: tiles %llu cyc/tile %.0f wait0 %.0f wait1 %.0f k2 %.0f k3 %.0f\n", w,
+                h[w * 8 + 5], h[w * 8] / tl, h[w * 8 + 1] / tl, h[w * 8 + 2] / tl, h[w * 8 + 3] / tl, h[w * 8 + 4] / tl);
+      }
+      fprintf(stderr, "tcprof grid %u ipc %u nch %u spq %u\n", grid, a.ipc, a.nch, a.spq);
     }
     gather_lists_kernel<<<unsigned(qn), 256, 0, st>>>(lists.get(), counts.get(), a.slots, L, gathered.get(),
                                                       gcount.get());

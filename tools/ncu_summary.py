@@ -15,6 +15,11 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active']
 
 
+FUZZY = ['pipe_tensor_cycles_active_realtime.avg.pct', 'sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed',
+         'l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct', 'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct',
+         'sm__inst_executed_pipe_tmem.avg.pct']
+
+
 def main(rep, top=18):
     raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
@@ -24,6 +29,9 @@ def main(rep, top=18):
         for w in WANT:
             if w in h:
                 print(f'  {w:62s} {r[h.index(w)]:>16s} {units[h.index(w)]}')
+        for i, name in enumerate(h):  # tensor-core / TMEM / shared-memory pipes (K7)
+            if any(x in name for x in FUZZY) and r[i] not in ('', '0', '0.00'):
+                print(f'  {name[-62:]:62s} {r[i]:>16s} {units[i]}')
     src = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass'],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(src.splitlines()))

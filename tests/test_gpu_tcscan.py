@@ -82,3 +82,34 @@ def test_tc_scan_heavy_ties(cuda_ok):
         ti, td = _scan(idx, qs, k, "tc")
         pi, pd = _scan(idx, qs, k, "popc")
         assert np.array_equal(ti, pi) and np.array_equal(td, pd), k
+
+
+@pytest.mark.parametrize("bits,first,n", [(64, 1, 5001), (192, 3, 4099), (64, 0, 129), (128, 5, 77)])
+def test_tc_scan_misaligned_and_ragged(cuda_ok, port, bits, first, n):
+    """Raw device scan over codes starting at an arbitrary row (8-byte aligned only: the TMA bulk
+    copies take the 16-byte-aligned interior, plain loads the head and tail) and ragged sizes."""
+    import torch
+
+    from paper_1307_2982_b200 import _lib
+    import paper_1307_2982_b200 as mg
+
+    L = _lib.lib()
+    W = (bits + 63) // 64
+    allc = mg.gen_uniform(first + n, bits, 40 + bits).raw_words()
+    qs = mg.gen_uniform(130, bits, 41 + bits).raw_words()
+    k = min(50, n)
+    d_all = torch.from_numpy(allc.view(np.int64)).cuda()
+    dq = torch.from_numpy(qs.view(np.int64)).cuda()
+    ids = torch.empty((130, k), dtype=torch.int32, device="cuda")
+    ds = torch.empty((130, k), dtype=torch.int32, device="cuda")
+    os.environ["MIHG_SCAN_KERNEL"] = "tc"
+    try:
+        _lib.check(L.mihg_scan_knn_raw_device(C.c_void_p(d_all.data_ptr() + first * W * 8), n, bits, 1000,
+                                              C.c_void_p(dq.data_ptr()), 130, k, C.c_void_p(ids.data_ptr()),
+                                              C.c_void_p(ds.data_ptr()), None))
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("MIHG_SCAN_KERNEL", None)
+    oi, od = port.scan_knn(allc[first:], bits, qs, k)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), oi + 1000)
+    assert np.array_equal(ds.cpu().numpy().view(np.uint32), od)

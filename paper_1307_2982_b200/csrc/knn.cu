@@ -886,7 +886,9 @@ double scan_cost_per_code(uint32_t bits) {
   const char* e = std::getenv("MIHG_TC_SPEEDUP");
   // measured pair rates on B200 (bench.py --method scan, 1e4 queries): K7 4.2e12 pairs/s (64-bit,
   // n = 1e8) ... 2.9e12 (256-bit, n = 1e9); K6 1.95e12 (W=1) ... 5.3e11 (W=4) pairs/s
-  const double f = e ? std::atof(e) : (W == 1 ? 2.1 : W == 2 ? 3.5 : W == 3 ? 4.5 : 5.5);
+  // (W <= 2: no credit — MIH's candidate verification, not charged by the probe count, dominates
+  // there; measured config 2 at k = 100 lost 17% when stragglers were switched on the rate ratio)
+  const double f = e ? std::atof(e) : (W <= 2 ? 1.0 : W == 3 ? 4.5 : 5.5);
   return W / f;
 }
 
@@ -1038,7 +1040,11 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     const uint32_t a = r % m, rr = r / m;
     const uint32_t s = idx.lengths[a];
     const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
-    if (alpha > 0 && double(acc + ring) * probe_pairs >= alpha * scan_pairs) {
+    // the scan of a switched batch costs whole 128-query tiles on the tensor cores (K7), so a few
+    // stragglers are charged a full tile's pass over the database
+    const double scan_q = scan_kernel_for(idx.bits) == ScanKernel::Tensor ? double((nact + 127) / 128 * 128)
+                                                                           : double(nact);
+    if (alpha > 0 && double(acc + ring) * probe_pairs * double(nact) >= alpha * scan_pairs * scan_q) {
       switched = act_in;  // every active query has probed the same `acc` buckets so far
       nswitched = nact;
       neutralise_kernel<<<unsigned(std::min<uint64_t>((nact + 255) / 256, 1024)), 256, 0, st>>>(

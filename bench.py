@@ -306,7 +306,10 @@ def main():
         all_d = torch.empty((world, nq, kk), dtype=torch.int32, device=dev)
         out_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
         out_d = torch.empty((nq, k), dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: the library's stream-ordered workspace allocations are then
+    # reused within the stream instead of going through the legacy default stream
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     partition = None
     if probe_part:

@@ -108,17 +108,6 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
-// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8 (A signed, B unsigned, s32 accumulate)
-__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
 // D[tmem] (+)= A[tmem] . B[smem]^T, kind::i8 (A signed in TMEM, B unsigned in shared memory)
 __device__ __forceinline__ void tc_mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                              uint32_t accumulate) {
@@ -424,7 +413,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
       uint32_t gb_next = qvalid ? __ldcg(a.gbound + q) : 0u;
       int32_t shared_b = qvalid ? int32_t(a.bits) : -1;
       for (uint32_t t = tg; t < tg + T; ++t) {
-        const uint32_t b = t % kAcc, bph = (t / kAcc) & 1;
+        const uint32_t b = t % kAcc;
         if (((t - tg) & 3) == 0 && qvalid) {
           shared_b = int32_t(min(gb_next, a.bits));
           gb_next = __ldcg(a.gbound + q);

@@ -54,6 +54,30 @@ mihg::Index& impl(const mihg_index* idx) {
   return *idx->impl;
 }
 
+// Runs the index's work on its own stream, ordered after / before the caller's stream with events:
+// the library's stream-ordered workspace allocations then always live on one stream (cross-stream
+// frees defeat the pool's reuse; measured: config 4 k=1000 through a caller stream 112-211K q/s vs
+// 233K through the index stream).
+struct StreamJoin {
+  cudaStream_t user, own;
+  explicit StreamJoin(cudaStream_t user_stream, cudaStream_t index_stream) : user(user_stream), own(index_stream) {
+    if (user == own) return;
+    cudaEvent_t e;
+    MIHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    MIHG_CUDA(cudaEventRecord(e, user));
+    MIHG_CUDA(cudaStreamWaitEvent(own, e, 0));
+    cudaEventDestroy(e);
+  }
+  ~StreamJoin() {
+    if (user == own) return;
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+    cudaEventRecord(e, own);
+    cudaStreamWaitEvent(user, e, 0);
+    cudaEventDestroy(e);
+  }
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -258,8 +282,8 @@ int mihg_knn_batch_device(mihg_index* idx, const uint64_t* d_queries, uint64_t n
     mihg::Index& ix = impl(idx);
     DeviceGuard g(ix.device);
     std::lock_guard<std::mutex> lk(ix.mu);
-    mihg::knn_device(ix, d_queries, nq, k, d_ids, d_dists, reinterpret_cast<mihg::Trace*>(d_traces),
-                     static_cast<cudaStream_t>(stream));
+    StreamJoin j(static_cast<cudaStream_t>(stream), ix.stream);
+    mihg::knn_device(ix, d_queries, nq, k, d_ids, d_dists, reinterpret_cast<mihg::Trace*>(d_traces), ix.stream);
   });
 }
 
@@ -280,8 +304,9 @@ int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint6
     }
     mihg::KnnOptions opt;
     opt.part = part ? &pt : nullptr;
-    mihg::knn_device(ix, d_queries, nq, k, d_ids, d_dists, reinterpret_cast<mihg::Trace*>(d_traces),
-                     static_cast<cudaStream_t>(stream), opt);
+    StreamJoin j(static_cast<cudaStream_t>(stream), ix.stream);
+    mihg::knn_device(ix, d_queries, nq, k, d_ids, d_dists, reinterpret_cast<mihg::Trace*>(d_traces), ix.stream,
+                     opt);
   });
 }
 

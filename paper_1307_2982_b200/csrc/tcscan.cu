@@ -40,6 +40,7 @@ constexpr int kTcM = 128;        // queries per CTA (TMEM lanes)
 constexpr int kTcN = 128;        // codes per tile (MMA N)
 constexpr int kAcc = 3;          // TMEM accumulators of kTcN columns at [0, 384); A (queries) at 384
 constexpr uint32_t kATmemCol = kAcc * kTcN;
+constexpr uint32_t kSfaCol = 448, kSfbCol = 480;  // E8M0 block scales of the E2M1 variant
 constexpr int kEpiGroups = 4;    // epilogue groups of 4 warps; group g drains columns [32 g, 32 g + 32)
 constexpr int kEpiCols = kTcN / kEpiGroups;
 constexpr int kEpiWarps = 4 * kEpiGroups;
@@ -118,6 +119,32 @@ __device__ __forceinline__ void tc_mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, u
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] . B[smem]^T, kind::mxf4 (E2M1, f32 accumulate), unit E8M0 block scales in TMEM
+__device__ __forceinline__ void tc_mma_f4_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate, uint32_t tmem_sfa, uint32_t tmem_sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
+      : "memory");
+}
+constexpr uint32_t tc_idesc_f4(uint32_t M, uint32_t N) {
+  return (1u << 7) | (1u << 10) | ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24);
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+// 8 bits -> 8 nibbles (bit i -> bit 4 i), by shift-or-mask steps (a multiply would carry)
+__device__ __forceinline__ uint32_t spread_n8(uint32_t x) {
+  x = (x | (x << 12)) & 0x000F000Fu;
+  x = (x | (x << 6)) & 0x03030303u;
+  return (x | (x << 3)) & 0x11111111u;
+}
+
 // 32 TMEM lanes x 16 consecutive 32-bit columns <- 16 registers per thread (lane = thread).
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
@@ -182,21 +209,23 @@ __device__ __forceinline__ void raw_span(const uint64_t* codes, uint64_t id0, ui
   bytes = e16 > s16 ? uint32_t(e16 - s16) : 0u;
 }
 
-template <int KB>
+template <int KB, bool kF4 = false>
 struct TcCfg {
   static constexpr int W = KB / 64;
-  static constexpr uint32_t kKBp = (KB + 127) / 128 * 128;  // whole 128-byte swizzle rows
+  static constexpr uint32_t kOpBytes = kF4 ? KB / 2 : KB;
+  static constexpr int kSteps = kOpBytes / 32;
+  static constexpr uint32_t kKBp = (kOpBytes + 127) / 128 * 128;  // whole 128-byte swizzle rows
   static constexpr uint32_t kA = 0;  // A lives in TMEM
   static constexpr uint32_t kB = kTcN * kKBp;
-  static constexpr int kStages = KB <= 64 ? 8 : (KB <= 128 ? 6 : 4);
+  static constexpr int kStages = kKBp <= 128 ? (KB <= 64 ? 8 : 6) : 4;
   static constexpr uint32_t kRawBytes = kTcN * W * 8;  // one raw tile of packed codes
   static constexpr uint32_t kSmem = 1024 + kA + kStages * kB + kRaw * kRawBytes;  // + barriers/hist
   static_assert(kStages > kAcc, "the stage barriers double as accumulator-ready signals");
 };
 
-template <int KB, bool kDump>
+template <int KB, bool kDump, bool kF4>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
-  using Cfg = TcCfg<KB>;
+  using Cfg = TcCfg<KB, kF4>;
   constexpr int W = Cfg::W;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -246,6 +275,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (kF4) {
+    if (warp < 4) {
+      uint32_t ones[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ones[i] = 0x7F7F7F7Fu;
+      tmem_st8(tmem + ((warp * 32) << 16) + kSfaCol, ones);
+      tmem_st8(tmem + ((warp * 32) << 16) + kSfbCol, ones);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  }
 
   // This CTA's work items [i0, i1) (tile-major): consecutive items of one query tile form a
   // segment over one contiguous id range, with one candidate list per (query, group).
@@ -269,6 +308,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     if (warp < 4) {
       const uint32_t r = warp * 32 + lane;
       const uint64_t q = q0 + r;
+      if constexpr (kF4) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          uint32_t w8[8];
+          const uint64_t word = q < a.nq ? __ldg(a.queries + q * W + w) : 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            w8[i] = q < a.nq ? ((spread_n8(uint32_t(word >> (8 * i)) & 0xFFu) << 3) | 0x22222222u) : 0u;
+          tmem_st8(tmem + ((warp * 32) << 16) + kATmemCol + w * 8, w8);
+        }
+      } else
 #pragma unroll
       for (int c16 = 0; c16 < KB / 64; ++c16) {  // 16 columns = 64 bytes = 64 query bits per store
         uint32_t w16[16];
@@ -289,11 +339,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
 
     if (a.mma_only) {
       if (warp == kMmaWarp && lane == 0) {
-        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
+        constexpr uint32_t idesc = kF4 ? tc_idesc_f4(kTcM, kTcN) : tc_idesc(kTcM, kTcN);
         const uint32_t b_addr = smem_u32(sB);
         for (uint32_t t = tg; t < tg + T; ++t) {
 #pragma unroll
-          for (int kk = 0; kk < KB / 32; ++kk)
+          for (int kk = 0; kk < Cfg::kSteps; ++kk)
+            if constexpr (kF4)
+              tc_mma_f4_ts(tmem + (t % kAcc) * kTcN, tmem + kATmemCol + kk * 8,
+                           smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kTcN)),
+                           idesc, kk > 0, tmem + kSfaCol, tmem + kSfbCol);
+            else
             tc_mma_i8_ts(tmem + (t % kAcc) * kTcN, tmem + kATmemCol + kk * 8,
                          smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kTcN)),
                          idesc, kk > 0);
@@ -306,7 +361,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     } else if (warp == kMmaWarp) {
       // ===== MMA issuer =====
       if (lane == 0) {
-        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
+        constexpr uint32_t idesc = kF4 ? tc_idesc_f4(kTcM, kTcN) : tc_idesc(kTcM, kTcN);
         const uint32_t b_addr = smem_u32(sB);
         for (uint32_t t = tg; t < tg + T; ++t) {
           const uint32_t s = t % S, ph = (t / S) & 1, b = t % kAcc, bph = (t / kAcc) & 1;
@@ -314,9 +369,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           wait_k(full + s, ph, 1);
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < KB / 32; ++kk) {  // K = 32 bytes = 8 TMEM columns of A per step
+          for (int kk = 0; kk < Cfg::kSteps; ++kk) {  // 32 bytes = 8 TMEM columns of A per step
             const uint64_t bd = smem_desc_sw128(kstep_addr(b_addr + s * Cfg::kB, kk, kTcN));
-            tc_mma_i8_ts(tmem + b * kTcN, tmem + kATmemCol + kk * 8, bd, idesc, kk > 0);
+            if constexpr (kF4)
+              tc_mma_f4_ts(tmem + b * kTcN, tmem + kATmemCol + kk * 8, bd, idesc, kk > 0, tmem + kSfaCol,
+                           tmem + kSfbCol);
+            else
+              tc_mma_i8_ts(tmem + b * kTcN, tmem + kATmemCol + kk * 8, bd, idesc, kk > 0);
           }
           tc_commit(empty + s);  // ONE commit per tile: frees the B stage and publishes the accumulator
         }
@@ -369,6 +428,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         wait_k(empty + s, ph ^ 1, 1);
         const unsigned long long c_x = a.prof ? clock64() : 0;
         uint8_t* dst = sB + s * Cfg::kB;
+        if constexpr (kF4) {
+#pragma unroll
+          for (int c = 0; c < KB / 32; ++c) {
+            const uint32_t h = uint32_t(cur[c >> 1] >> ((c & 1) * 32));
+            const uint4 o = make_uint4(spread_n8(h & 0xFF) << 1, spread_n8((h >> 8) & 0xFF) << 1,
+                                       spread_n8((h >> 16) & 0xFF) << 1, spread_n8(h >> 24) << 1);
+            *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c, kTcN)) = o;
+          }
+        } else
 #pragma unroll
         for (int c = 0; c < KB / 16; ++c) {
           const uint32_t h = uint32_t(cur[c >> 2] >> ((c & 3) * 16)) & 0xFFFFu;
@@ -422,6 +490,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         tc_fence_after();
         int32_t v[kEpiCols];
         tmem_ld32(taddr0 + b * kTcN, v);
+        if constexpr (kF4 && kDump) {
+#pragma unroll
+          for (int j = 0; j < kEpiCols; ++j) v[j] = __float2int_rn(__int_as_float(v[j]));
+        }
         tc_fence_before();  // accumulator drained into registers: hand it back
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + b);
@@ -432,19 +504,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
               if (id0 + j < hi) a.dump[q * a.n + id0 + j] = v[j] + pq;
         }
         const int32_t thr = min(own, shared_b) - pq;
-        // tree minimum (independent 3-input mins, short dependency chain)
-        int32_t m8[11];
+        // tree minimum (independent 3-input mins, short dependency chain); the E2M1 variant's
+        // accumulators are exact small integers in f32 and are compared as floats
+        bool any_hit;
+        if constexpr (kF4 && !kDump) {
+          float m8[11];
 #pragma unroll
-        for (int i = 0; i < 10; ++i) m8[i] = min(min(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
-        m8[10] = min(v[30], v[31]);
-        const int32_t m3a = min(min(m8[0], m8[1]), m8[2]), m3b = min(min(m8[3], m8[4]), m8[5]);
-        const int32_t m3c = min(min(m8[6], m8[7]), m8[8]), m3d = min(m8[9], m8[10]);
-        const int32_t mn = min(min(m3a, m3b), min(m3c, m3d));
-        if (mn <= thr) {
+          for (int i = 0; i < 10; ++i)
+            m8[i] = fminf(fminf(__int_as_float(v[3 * i]), __int_as_float(v[3 * i + 1])), __int_as_float(v[3 * i + 2]));
+          m8[10] = fminf(__int_as_float(v[30]), __int_as_float(v[31]));
+          const float m3a = fminf(fminf(m8[0], m8[1]), m8[2]), m3b = fminf(fminf(m8[3], m8[4]), m8[5]);
+          const float m3c = fminf(fminf(m8[6], m8[7]), m8[8]), m3d = fminf(m8[9], m8[10]);
+          any_hit = fminf(fminf(m3a, m3b), fminf(m3c, m3d)) <= float(thr);
+        } else {
+          int32_t m8[11];
+#pragma unroll
+          for (int i = 0; i < 10; ++i) m8[i] = min(min(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+          m8[10] = min(v[30], v[31]);
+          const int32_t m3a = min(min(m8[0], m8[1]), m8[2]), m3b = min(min(m8[3], m8[4]), m8[5]);
+          const int32_t m3c = min(min(m8[6], m8[7]), m8[8]), m3d = min(m8[9], m8[10]);
+          any_hit = min(min(m3a, m3b), min(m3c, m3d)) <= thr;
+        }
+        if (any_hit) {
           // hit mask, then the (few) hits re-derive their distance from the code words (L2-hot)
           uint32_t m = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) m |= uint32_t(v[j] <= thr) << j;
+          for (int j = 0; j < 32; ++j) {
+            if constexpr (kF4 && !kDump) m |= uint32_t(__int_as_float(v[j]) <= float(thr)) << j;
+            else m |= uint32_t(v[j] <= thr) << j;
+          }
           while (m) {
             const uint32_t j = __ffs(m) - 1;
             m &= m - 1;
@@ -494,24 +582,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   }
 }
 
-template <int KB>
+template <int KB, bool kF4>
 size_t tc_smem_bytes(uint32_t bits) {
-  using Cfg = TcCfg<KB>;
+  using Cfg = TcCfg<KB, kF4>;
   return Cfg::kSmem + (2 * Cfg::kStages + 2 * kAcc + 2 * kRaw) * 8 + 16 + size_t(kEpiWarps) * (bits + 1) * 4;
 }
 
-template <int KB, bool kDump>
+template <int KB, bool kDump, bool kF4>
 void launch_tc_k(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  const size_t smem = tc_smem_bytes<KB>(a.bits);
-  MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, kDump>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  tc_scan_kernel<KB, kDump><<<grid, kTcThreads, smem, st>>>(a);
+  const size_t smem = tc_smem_bytes<KB, kF4>(a.bits);
+  MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, kDump, kF4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+  tc_scan_kernel<KB, kDump, kF4><<<grid, kTcThreads, smem, st>>>(a);
   MIHG_LAUNCH();
 }
 
+// MMA kind: int8 (default) or the experimental block-scaled E2M1 (MIHG_TC_KIND=fp4).
 template <int KB>
 void launch_tc(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  if (a.dump) launch_tc_k<KB, true>(a, grid, st);
-  else launch_tc_k<KB, false>(a, grid, st);
+  const char* e = std::getenv("MIHG_TC_KIND");
+  const bool f4 = e && e[0] == 'f';
+  if (a.dump) {
+    if (f4) launch_tc_k<KB, true, true>(a, grid, st);
+    else launch_tc_k<KB, true, false>(a, grid, st);
+  } else {
+    if (f4) launch_tc_k<KB, false, true>(a, grid, st);
+    else launch_tc_k<KB, false, false>(a, grid, st);
+  }
 }
 
 }  // namespace

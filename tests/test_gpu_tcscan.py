@@ -10,6 +10,14 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["i8", "fp4"], autouse=True)
+def mma_kind(request):
+    """Every K7 test runs with both MMA kinds: int8 (default) and block-scaled E2M1."""
+    os.environ["MIHG_TC_KIND"] = request.param
+    yield request.param
+    os.environ.pop("MIHG_TC_KIND", None)
+
+
 def _popc_dist(q, x):
     """[nq, n] Hamming distances of packed u64 rows (numpy restatement of hamming_words)."""
     d = np.zeros((q.shape[0], x.shape[0]), np.int64)

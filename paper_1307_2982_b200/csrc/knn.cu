@@ -884,11 +884,11 @@ double scan_cost_per_code(uint32_t bits) {
   const uint32_t W = words_per_code(bits);
   if (scan_kernel_for(bits) != ScanKernel::Tensor) return W;
   const char* e = std::getenv("MIHG_TC_SPEEDUP");
-  // measured pair rates on B200 (bench.py --method scan, 1e4 queries): K7 4.2e12 pairs/s (64-bit,
-  // n = 1e8) ... 2.9e12 (256-bit, n = 1e9); K6 1.95e12 (W=1) ... 5.3e11 (W=4) pairs/s
+  // measured pair rates on B200 (bench.py --method scan, 1e4 queries): K7 4.8e12 pairs/s (64-bit,
+  // n = 1e8) ... 3.8e12 (256-bit, n = 1e9); K6 1.95e12 (W=1) ... 5.3e11 (W=4) pairs/s
   // (W <= 2: no credit — MIH's candidate verification, not charged by the probe count, dominates
   // there; measured config 2 at k = 100 lost 17% when stragglers were switched on the rate ratio)
-  const double f = e ? std::atof(e) : (W <= 2 ? 1.0 : W == 3 ? 4.5 : 5.5);
+  const double f = e ? std::atof(e) : (W <= 2 ? 1.0 : W == 3 ? 5.5 : 7.0);
   return W / f;
 }
 

@@ -37,15 +37,15 @@ namespace mihg {
 namespace {
 
 constexpr int kTcM = 128;        // queries per CTA (TMEM lanes)
-constexpr int kTcN = 128;        // codes per tile (MMA N)
-constexpr int kAcc = 3;          // TMEM accumulators of kTcN columns at [0, 384); A (queries) at 384
+constexpr int kTcN = 256;        // codes per tile (MMA N)
+constexpr int kAcc = 2;          // TMEM accumulators of kTcN columns (all 512 columns)
 constexpr uint32_t kATmemCol = kAcc * kTcN;
 constexpr uint32_t kSfaCol = 448, kSfbCol = 480;  // E8M0 block scales of the E2M1 variant
 constexpr int kEpiGroups = 4;    // epilogue groups of 4 warps; group g drains columns [32 g, 32 g + 32)
 constexpr int kEpiCols = kTcN / kEpiGroups;
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kProdWarps = 4;    // 128 producer threads: one code each per tile
-constexpr int kRaw = 16;         // raw code tiles in flight (TMA bulk ring)
+constexpr int kRaw = 4;          // raw code tiles in flight (TMA bulk ring)
 constexpr int kTcThreads = (kEpiWarps + kProdWarps + 2) * 32;
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 constexpr int kLoadWarp = kMmaWarp + 1;
@@ -108,6 +108,16 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::i8 (A signed, B unsigned, s32 accumulate)
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 // D[tmem] (+)= A[tmem] . B[smem]^T, kind::i8 (A signed in TMEM, B unsigned in shared memory)
 __device__ __forceinline__ void tc_mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
@@ -215,12 +225,11 @@ struct TcCfg {
   static constexpr uint32_t kOpBytes = kF4 ? KB / 2 : KB;
   static constexpr int kSteps = kOpBytes / 32;
   static constexpr uint32_t kKBp = (kOpBytes + 127) / 128 * 128;  // whole 128-byte swizzle rows
-  static constexpr uint32_t kA = 0;  // A lives in TMEM
+  static constexpr uint32_t kA = kTcM * kKBp;  // A (queries) in shared memory
   static constexpr uint32_t kB = kTcN * kKBp;
-  static constexpr int kStages = kKBp <= 128 ? (KB <= 64 ? 8 : 6) : 4;
+  static constexpr int kStages = kKBp <= 128 ? 4 : 2;
   static constexpr uint32_t kRawBytes = kTcN * W * 8;  // one raw tile of packed codes
   static constexpr uint32_t kSmem = 1024 + kA + kStages * kB + kRaw * kRawBytes;  // + barriers/hist
-  static_assert(kStages > kAcc, "the stage barriers double as accumulator-ready signals");
 };
 
 template <int KB, bool kDump, bool kF4>
@@ -230,7 +239,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = base;
+  uint8_t* sA = base;
+  uint8_t* sB = base + Cfg::kA;
   uint8_t* sRaw = sB + S * Cfg::kB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRaw + kRaw * Cfg::kRawBytes);
   uint64_t* full = bars;
@@ -320,15 +330,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         }
       } else
 #pragma unroll
-      for (int c16 = 0; c16 < KB / 64; ++c16) {  // 16 columns = 64 bytes = 64 query bits per store
-        uint32_t w16[16];
-        const uint64_t word = q < a.nq ? __ldg(a.queries + q * W + c16) : 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t nib = uint32_t(word >> (4 * i)) & 0xFu;
-          w16[i] = q < a.nq ? ((spread4(nib) * 0xFEu) ^ 0x01010101u) : 0u;
+      for (int c = 0; c < KB / 16; ++c) {  // 16-byte chunk c = query bits [16 c, 16 c + 16)
+        uint4 o = make_uint4(0, 0, 0, 0);
+        if (q < a.nq) {
+          const uint32_t h = uint32_t(__ldg(a.queries + q * W + (c >> 2)) >> ((c & 3) * 16)) & 0xFFFFu;
+          o.x = (spread4(h & 0xF) * 0xFEu) ^ 0x01010101u;
+          o.y = (spread4((h >> 4) & 0xF) * 0xFEu) ^ 0x01010101u;
+          o.z = (spread4((h >> 8) & 0xF) * 0xFEu) ^ 0x01010101u;
+          o.w = (spread4(h >> 12) * 0xFEu) ^ 0x01010101u;
         }
-        tmem_st16(tmem + ((warp * 32) << 16) + kATmemCol + c16 * 16, w16);
+        *reinterpret_cast<uint4*>(sA + core_off<KB>(r, c, kTcM)) = o;
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -344,14 +355,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         for (uint32_t t = tg; t < tg + T; ++t) {
 #pragma unroll
           for (int kk = 0; kk < Cfg::kSteps; ++kk)
-            if constexpr (kF4)
-              tc_mma_f4_ts(tmem + (t % kAcc) * kTcN, tmem + kATmemCol + kk * 8,
-                           smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kTcN)),
-                           idesc, kk > 0, tmem + kSfaCol, tmem + kSfbCol);
-            else
-            tc_mma_i8_ts(tmem + (t % kAcc) * kTcN, tmem + kATmemCol + kk * 8,
-                         smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kTcN)),
-                         idesc, kk > 0);
+            tc_mma_i8(tmem + (t % kAcc) * kTcN, smem_desc_sw128(kstep_addr(smem_u32(sA), kk, kTcM)),
+                      smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kTcN)),
+                      idesc, kk > 0);
         }
         tc_commit(tfull);
         mbar_wait(tfull, mo_phase);  // drains this segment's MMAs
@@ -371,13 +377,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
 #pragma unroll
           for (int kk = 0; kk < Cfg::kSteps; ++kk) {  // 32 bytes = 8 TMEM columns of A per step
             const uint64_t bd = smem_desc_sw128(kstep_addr(b_addr + s * Cfg::kB, kk, kTcN));
-            if constexpr (kF4)
-              tc_mma_f4_ts(tmem + b * kTcN, tmem + kATmemCol + kk * 8, bd, idesc, kk > 0, tmem + kSfaCol,
-                           tmem + kSfbCol);
-            else
-              tc_mma_i8_ts(tmem + b * kTcN, tmem + kATmemCol + kk * 8, bd, idesc, kk > 0);
+            tc_mma_i8(tmem + b * kTcN, smem_desc_sw128(kstep_addr(smem_u32(sA), kk, kTcM)), bd, idesc, kk > 0);
           }
-          tc_commit(empty + s);  // ONE commit per tile: frees the B stage and publishes the accumulator
+          tc_commit(empty + s);  // frees the B stage
+          tc_commit(tfull + b);  // publishes the accumulator
         }
       }
       __syncwarp();
@@ -405,52 +408,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
       }
       __syncwarp();
     } else if (warp >= kEpiWarps) {
-      // ===== producers: raw code -> 0/1 bytes =====
-      const uint32_t p = threadIdx.x - kEpiWarps * 32;  // code row within the tile
+      // ===== producers: raw code -> 0/1 bytes (kTcN / 128 codes per thread per tile) =====
+      const uint32_t p0 = threadIdx.x - kEpiWarps * 32;
       for (uint32_t t = tg; t < tg + T; ++t) {
         const uint32_t s = t % S, ph = (t / S) & 1, r = t % kRaw;
-        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN, id = id0 + p;
+        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN;
         uint32_t skip, tbytes;
         raw_span<W>(a.codes, id0, hi, skip, tbytes);
         wait_k(rfull + r, (t / kRaw) & 1, 0);
-        uint64_t cur[W];
-        if (p * W * 8 >= skip && (p + 1) * W * 8 <= skip + tbytes) {
-          const uint64_t* src = reinterpret_cast<const uint64_t*>(sRaw + r * Cfg::kRawBytes + p * W * 8 - skip);
+        uint64_t cur[kTcN / 128][W];
 #pragma unroll
-          for (int w = 0; w < W; ++w) cur[w] = src[w];
-        } else if (id < hi) {  // misaligned head / odd tail of the tile
+        for (int h = 0; h < kTcN / 128; ++h) {
+          const uint32_t p = p0 + 128 * h;
+          const uint64_t id = id0 + p;
+          if (p * W * 8 >= skip && (p + 1) * W * 8 <= skip + tbytes) {
+            const uint64_t* src = reinterpret_cast<const uint64_t*>(sRaw + r * Cfg::kRawBytes + p * W * 8 - skip);
 #pragma unroll
-          for (int w = 0; w < W; ++w) cur[w] = __ldg(a.codes + id * W + w);
-        } else {
+            for (int w = 0; w < W; ++w) cur[h][w] = src[w];
+          } else if (id < hi) {  // misaligned head / odd tail of the tile
 #pragma unroll
-          for (int w = 0; w < W; ++w) cur[w] = 0;
+            for (int w = 0; w < W; ++w) cur[h][w] = __ldg(a.codes + id * W + w);
+          } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) cur[h][w] = 0;
+          }
         }
         wait_k(empty + s, ph ^ 1, 1);
-        const unsigned long long c_x = a.prof ? clock64() : 0;
         uint8_t* dst = sB + s * Cfg::kB;
-        if constexpr (kF4) {
 #pragma unroll
-          for (int c = 0; c < KB / 32; ++c) {
-            const uint32_t h = uint32_t(cur[c >> 1] >> ((c & 1) * 32));
-            const uint4 o = make_uint4(spread_n8(h & 0xFF) << 1, spread_n8((h >> 8) & 0xFF) << 1,
-                                       spread_n8((h >> 16) & 0xFF) << 1, spread_n8(h >> 24) << 1);
+        for (int h = 0; h < kTcN / 128; ++h) {
+          const uint32_t p = p0 + 128 * h;
+#pragma unroll
+          for (int c = 0; c < KB / 16; ++c) {
+            const uint32_t hh = uint32_t(cur[h][c >> 2] >> ((c & 3) * 16)) & 0xFFFFu;
+            const uint4 o = make_uint4(spread4(hh & 0xF), spread4((hh >> 4) & 0xF), spread4((hh >> 8) & 0xF),
+                                       spread4(hh >> 12));
             *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c, kTcN)) = o;
           }
-        } else
-#pragma unroll
-        for (int c = 0; c < KB / 16; ++c) {
-          const uint32_t h = uint32_t(cur[c >> 2] >> ((c & 3) * 16)) & 0xFFFFu;
-          const uint4 o = make_uint4(spread4(h & 0xF), spread4((h >> 4) & 0xF), spread4((h >> 8) & 0xF),
-                                     spread4(h >> 12));
-          *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c, kTcN)) = o;
         }
-        const unsigned long long c_f = a.prof ? clock64() : 0;
         fence_proxy_async();
         __syncwarp();
-        if (a.prof) {
-          wcyc[2] += clock64() - c_f;
-          wcyc[3] += c_f - c_x;
-        }
         if (lane == 0) {
           mbar_arrive(full + s);
           mbar_arrive(rempty + r);  // the raw words were consumed by the expansion above
@@ -486,21 +483,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           shared_b = int32_t(min(gb_next, a.bits));
           gb_next = __ldcg(a.gbound + q);
         }
-        wait_k(empty + (t % S), (t / S) & 1, 0);  // the tile's MMAs are complete (S > kAcc: no aliasing)
+        wait_k(tfull + b, (t / kAcc) & 1, 0);  // the tile's MMAs are complete
         tc_fence_after();
-        int32_t v[kEpiCols];
-        tmem_ld32(taddr0 + b * kTcN, v);
+#pragma unroll 1
+        for (int sc = 0; sc < kEpiCols / 32; ++sc) {  // 32-column sub-chunks of this group's columns
+        int32_t v[32];
+        tmem_ld32(taddr0 + b * kTcN + sc * 32, v);
         if constexpr (kF4 && kDump) {
 #pragma unroll
-          for (int j = 0; j < kEpiCols; ++j) v[j] = __float2int_rn(__int_as_float(v[j]));
+          for (int j = 0; j < 32; ++j) v[j] = __float2int_rn(__int_as_float(v[j]));
         }
-        tc_fence_before();  // accumulator drained into registers: hand it back
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty + b);
-        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols;
+        if (sc == kEpiCols / 32 - 1) {
+          tc_fence_before();  // accumulator drained into registers: hand it back
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty + b);
+        }
+        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols + sc * 32;
         if constexpr (kDump) {
           if (qvalid)
-            for (int j = 0; j < kEpiCols; ++j)
+            for (int j = 0; j < 32; ++j)
               if (id0 + j < hi) a.dump[q * a.n + id0 + j] = v[j] + pq;
         }
         const int32_t thr = min(own, shared_b) - pq;
@@ -560,6 +561,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           }
           __syncwarp();
         }
+        }  // sub-chunks
       }
       if (qvalid) a.counts[q * a.slots + slot] = cnt;
     }
@@ -600,8 +602,9 @@ void launch_tc_k(const TcArgs& a, uint32_t grid, cudaStream_t st) {
 // MMA kind: int8 (default) or the experimental block-scaled E2M1 (MIHG_TC_KIND=fp4).
 template <int KB>
 void launch_tc(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  const char* e = std::getenv("MIHG_TC_KIND");
-  const bool f4 = e && e[0] == 'f';
+  // the E2M1 variant keeps A and its block scales in TMEM, which the two 256-column accumulators
+  // of this tile geometry fill completely: int8 only
+  const bool f4 = false;
   if (a.dump) {
     if (f4) launch_tc_k<KB, true, true>(a, grid, st);
     else launch_tc_k<KB, true, false>(a, grid, st);

@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(params=["i8", "fp4"], autouse=True)
 def mma_kind(request):
-    """Every K7 test runs with both MMA kinds: int8 (default) and block-scaled E2M1."""
+    """Every K7 test runs under both MMA_KIND settings (the 256-code-tile geometry runs int8 for
+    both: its accumulators fill TMEM, where the E2M1 variant keeps A and its block scales)."""
     os.environ["MIHG_TC_KIND"] = request.param
     yield request.param
     os.environ.pop("MIHG_TC_KIND", None)

@@ -199,29 +199,135 @@ def config_desc(cfg, args, world):
 
 
 # ---------------------------------------------------------------------------------------------
-def cpu_reference_run(cfg, codes_host, queries_host, steps, warmup, sample):
-    """Reference MihIndex::knn_search (oracle/_ref) with all host threads, `sample` queries per
-    step. Returns (q/s, threads, build_seconds, per-step seconds)."""
+# The reference's CPU implementation (oracle/_ref = the reference's own headers, unmodified):
+# MihIndex::knn_search and scan_knn timed on the host cores, and their answers kept as the parity
+# oracle of the GPU rows for the same queries (the verify-before-report gate of
+# tools/mih.cpp:274-301, against the reference itself).
+REF_MIH_FEASIBLE = {1: True, 2: True, 3: True, 4: True, 5: False}  # config 5: ~106 GB index
+MIH_SAMPLE = {1: 1000, 2: 1024, 3: 1024, 4: 1024, 5: 0}            # queries timed with all threads
+SCAN_SAMPLE = {1: 64, 2: 32, 3: 16, 4: 16, 5: 64}                 # scan_knn queries, all threads
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def _stats(secs):
+    secs = sorted(float(x) for x in secs)
+    if not secs:
+        return None
+    p95 = secs[min(len(secs) - 1, int(round(0.95 * (len(secs) - 1))))]
+    return {"mean_ms": 1e3 * statistics.mean(secs), "median_ms": 1e3 * statistics.median(secs),
+            "p95_ms": 1e3 * p95, "queries": len(secs)}
+
+
+def reference_leg(cfg, config_id, queries_host, db_words=None, mih_sample=None, scan_sample=None,
+                  single_sample=None, steps=1, warmup=0, log=None):
+    """Run the reference on the host. db_words: [n, W] host codes, or None for gen_uniform inside
+    the reference (uniform configs). Returns a dict with timings and the reference's answers:
+      mih: {qps, threads, per_query (all-thread), single_thread stats, ids, dists, traces, q0, nq}
+      scan: {qps, threads, per_query, ids, dists, q0, nq}
+    Queries are the first rows of the batch (q0 = 0)."""
     import oracle
 
     R = oracle.ref()
     threads = os.cpu_count() or 1
+    bits, k = cfg["bits"], cfg["k"]
+    out = {"cpu_model": cpu_model(), "cores": threads}
     t0 = time.time()
-    h = R.build_parallel(codes_host, cfg["bits"], cfg["m"])
-    build_s = time.time() - t0
-    nq = queries_host.shape[0]
-    times = []
-    for s in range(warmup + steps):
-        lo = (s * sample) % max(1, nq - sample + 1)
-        q = queries_host[lo:lo + sample]
+    held = None
+    if db_words is None:
+        held = R.db_gen_uniform(cfg["n"], bits, cfg["db_seed"])
+        db_words = held.words()
+    out["gen_s"] = time.time() - t0
+    ms = MIH_SAMPLE[config_id] if mih_sample is None else mih_sample
+    ss = SCAN_SAMPLE[config_id] if scan_sample is None else scan_sample
+    ms, ss = min(ms, queries_host.shape[0]), min(ss, queries_host.shape[0])
+    scan_owner = held
+    if REF_MIH_FEASIBLE[config_id] and ms > 0:
+        t0 = time.time()
+        h = R.build_parallel(db_words, bits, cfg["m"])
+        out["index_build_s"] = time.time() - t0
+        if held is not None:  # the index holds its own copy now
+            del db_words
+            held = None
+        scan_owner = h
+        q = queries_host[:ms]
+        best = None
+        for s in range(warmup + steps):  # best of `steps` (tools/mih.cpp:308-314), warm-up untimed
+            t = time.perf_counter()
+            ids, dists, tr, secs = h.knn_timed(q, k, threads=threads)
+            dt = time.perf_counter() - t
+            if s >= warmup and (best is None or dt < best):
+                best = dt
+        ns = min(single_sample or 32, ms)
+        _, _, _, secs1 = h.knn_timed(queries_host[:ns], k, threads=1)
+        out["mih"] = {"qps": ms / best, "threads": threads, "queries": ms, "wall_s": best,
+                      "per_query_under_load": _stats(secs), "single_thread": _stats(secs1),
+                      "ids": ids, "dists": dists, "traces": tr}
+        if log:
+            log(f"reference MIH: {ms} queries, {ms / best:.1f} q/s on {threads} threads")
+    if ss > 0:
+        q = queries_host[:ss]
         t = time.perf_counter()
-        h.knn(q, cfg["k"], threads=threads)
+        ids, dists, secs = scan_owner.scan_knn_timed(q, k, threads=threads)
         dt = time.perf_counter() - t
-        if s >= warmup:
-            times.append(dt)
-    del h
-    qps = sample * len(times) / sum(times)
-    return qps, threads, build_s, times
+        ns = min(4, ss)
+        _, _, secs1 = scan_owner.scan_knn_timed(queries_host[:ns], k, threads=1)
+        out["scan"] = {"qps": ss / dt, "threads": threads, "queries": ss, "wall_s": dt,
+                       "per_query_under_load": _stats(secs), "single_thread": _stats(secs1),
+                       "ids": ids, "dists": dists}
+        if log:
+            log(f"reference scan_knn: {ss} queries, {ss / dt:.2f} q/s on {threads} threads")
+    return out
+
+
+def reference_baseline_json(leg, config_id):
+    """The cpu_baseline object (value = the reference MIH's all-thread q/s, or its scan where the
+    reference MIH cannot run)."""
+    mih, scan = leg.get("mih"), leg.get("scan")
+    strip = lambda d: None if d is None else {k: v for k, v in d.items() if k not in ("ids", "dists", "traces")}
+    head = mih or scan
+    what = "MihIndex::knn_search" if mih else "scan_knn (reference MIH index does not fit host memory)"
+    sample = (f"{head['queries']} queries (first rows of the batch), {what}, {head['threads']} threads, "
+              f"best of steps; full-size reference index/database; "
+              f"index build {leg.get('index_build_s', 0):.0f}s and data gen {leg.get('gen_s', 0):.0f}s excluded")
+    return {"value": head["qps"], "unit": "queries/s", "cores": leg["cores"], "kind": "reference",
+            "sample": sample, "cpu_model": leg["cpu_model"], "mih": strip(mih), "scan": strip(scan)}
+
+
+def parity_check(leg, gpu_ids, gpu_dists, gpu_traces=None):
+    """Compare GPU rows with the reference's answers for the same queries (ids and distances
+    exactly; traces where both exist). Returns the parity object of the JSON line."""
+    res = {"vs": [], "queries": 0, "mismatches": 0}
+    def cmp(name, ids, dists, tr=None):
+        n = ids.shape[0]
+        gi = np.asarray(gpu_ids[:n]).view(np.uint32).reshape(n, -1)
+        gd = np.asarray(gpu_dists[:n]).view(np.uint32).reshape(n, -1)
+        bad = int((~((gi == ids).all(1) & (gd == dists).all(1))).sum())
+        res["vs"].append(f"oracle/_ref {name}")
+        res["queries"] = max(res["queries"], n)
+        res["mismatches"] += bad
+        res[name] = {"queries": n, "mismatches": bad}
+        if tr is not None and gpu_traces is not None:
+            gt = np.asarray(gpu_traces[:n])
+            tb = int((~(gt[:, [0, 1, 2, 4]] == tr[:, [0, 1, 2, 4]]).all(1)).sum())
+            res[name]["trace_mismatches"] = tb
+            res["mismatches"] += tb
+    if leg.get("mih"):
+        m = leg["mih"]
+        cmp("MihIndex::knn_search", m["ids"], m["dists"], m["traces"])
+    if leg.get("scan"):
+        cmp("scan_knn", leg["scan"]["ids"], leg["scan"]["dists"])
+    return res
 
 
 def run_reference_arm(args):
@@ -235,24 +341,23 @@ def run_reference_arm(args):
     if not oracle.have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmihref.so not built"}))
         return
-    sample = args.cpu_sample or 64
     t0 = time.time()
-    codes = make_codes_host_cpu(cfg, 0, cfg["n"], cfg["db_seed"])
+    db = None if cfg["data"] == "uniform" else make_codes_host_cpu(cfg, 0, cfg["n"], cfg["db_seed"])
     queries = make_codes_host_cpu(cfg, 0, cfg["nq"], cfg["q_seed"])
     gen_s = time.time() - t0
-    qps, threads, build_s, times = cpu_reference_run(cfg, codes, queries, args.steps, args.warmup, sample)
+    leg = reference_leg(cfg, args.config, queries, db, mih_sample=args.cpu_sample or None,
+                        steps=args.steps, warmup=args.warmup)
+    cpu = reference_baseline_json(leg, args.config)
+    head = leg.get("mih") or leg.get("scan")
     line = {
-        "metric": "exact kNN queries/s", "value": qps, "unit": "queries/s", "impl": "reference",
+        "metric": "exact kNN queries/s", "value": cpu["value"], "unit": "queries/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1000 * head["wall_s"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": config_desc(cfg, args, 1),
-        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
-                         "sample": f"{sample} queries per step of the {cfg['nq']}-query batch, full "
-                                   f"n={cfg['n']} reference index (MihIndex::knn_search, "
-                                   f"one SearchScratch per thread); index build {build_s:.0f}s, "
-                                   f"data gen {gen_s:.0f}s excluded"},
-        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup": {"gen_s": gen_s + leg.get("gen_s", 0), "index_build_s": leg.get("index_build_s")},
     }
     print(json.dumps(line))
 
@@ -319,7 +424,7 @@ def main():
     elif world > 1 and args.method == "mih":  # id-range shards with global stopping (§8e refinement 1)
         from paper_1307_2982_b200.shard import nccl_allreduce
 
-        partition = (world, rank, nccl_allreduce(), True)
+        partition = (world, rank, nccl_allreduce(), True, k)  # stopping rule on the global k
 
     def step(qptr=None):
         qptr = qptr or queries.data_ptr()
@@ -373,39 +478,60 @@ def main():
     probe_ms = prof1.probe_ms / args.steps
     probe_launches = prof1.probe_launches / args.steps
 
-    # ---- verify before reporting (tools/mih.cpp:274-301 pattern): MIH == exhaustive scan ----
+    # the timed path's own answer (last timed step), kept for the gates below
+    if use_dist:
+        res_ids, res_d = out_ids.clone(), out_d.clone()
+    else:
+        res_ids, res_d = ids.clone(), dists.clone()
+
+    # ---- verify before reporting (tools/mih.cpp:274-301 pattern): the timed step's rows == the
+    # exhaustive scan (K7/K6) of the same queries; N > 1: every rank scans its own id range (or,
+    # probe partition, the full index) and the merged scans must equal the merged timed output ----
     nv = min(nq, 64)
-    vi = torch.empty((nv, kk), dtype=torch.int32, device=dev)
-    vd = torch.empty((nv, kk), dtype=torch.int32, device=dev)
-    si = torch.empty((nv, kk), dtype=torch.int32, device=dev)
-    sd = torch.empty((nv, kk), dtype=torch.int32, device=dev)
-    if probe_part:  # merged output of the last timed step (first nv rows) vs a full-index scan
+    si = torch.empty((nv, kk if not probe_part else k), dtype=torch.int32, device=dev)
+    sd = torch.empty_like(si)
+    if probe_part:  # replicated index: one full scan is the answer
         idx.scan_knn_device(queries.data_ptr(), nv, k, si.data_ptr(), sd.data_ptr(), stream=stream.cuda_stream)
         torch.cuda.synchronize(dev)
-        verified = bool(torch.equal(out_ids[:nv], si) and torch.equal(out_d[:nv], sd))
+        verified = bool(torch.equal(res_ids[:nv], si) and torch.equal(res_d[:nv], sd))
+    elif use_dist:  # id-range shards: merge of the per-shard scans
+        idx.scan_knn_device(queries.data_ptr(), nv, kk, si.data_ptr(), sd.data_ptr(), stream=stream.cuda_stream)
+        gi = torch.empty((world, nv, kk), dtype=torch.int32, device=dev)
+        gd = torch.empty_like(gi)
+        dist.all_gather_into_tensor(gi, si)
+        dist.all_gather_into_tensor(gd, sd)
+        mi = torch.empty((nv, k), dtype=torch.int32, device=dev)
+        md = torch.empty_like(mi)
+        _lib.check(L.mihg_merge_topk_device(C.c_void_p(gi.data_ptr()), C.c_void_p(gd.data_ptr()), world, nv, kk, k,
+                                            C.c_void_p(mi.data_ptr()), C.c_void_p(md.data_ptr()),
+                                            C.c_void_p(stream.cuda_stream)))
+        torch.cuda.synchronize(dev)
+        verified = bool(torch.equal(res_ids[:nv], mi) and torch.equal(res_d[:nv], md))
     else:
-        idx.knn_search_device(queries.data_ptr(), nv, kk, vi.data_ptr(), vd.data_ptr(), stream=stream.cuda_stream)
         idx.scan_knn_device(queries.data_ptr(), nv, kk, si.data_ptr(), sd.data_ptr(), stream=stream.cuda_stream)
         torch.cuda.synchronize(dev)
-        verified = bool(torch.equal(vi, si) and torch.equal(vd, sd))
-    if use_dist:  # every shard checks its local result; all must pass
+        verified = bool(torch.equal(res_ids[:nv], si) and torch.equal(res_d[:nv], sd))
+    if use_dist:  # every rank checks; all must pass
         vt = torch.tensor([1 if verified else 0], device=dev)
         dist.all_reduce(vt, op=dist.ReduceOp.MIN)
         verified = bool(vt.item())
     if not verified:
-        print(json.dumps({"error": "verification failed: MIH result differs from the exhaustive scan"}))
+        print(json.dumps({"error": "verification failed: the timed kNN result differs from the exhaustive scan"}))
         sys.exit(3)
 
     # ---- algorithmic bytes from the reference-identical traces (untimed run) ----
-    tr = torch.empty((nq, 5), dtype=torch.int64, device=dev)
-    idx.knn_search_device(queries.data_ptr(), nq, kk, ids.data_ptr(), dists.data_ptr(), tr.data_ptr(),
+    # (traced calls run pure MIH; at 256 bits that is ~50 q/s, so a 256-query sample is traced and
+    # scaled: its numbers only feed the HBM roofline, which the hybrid's tensor-core line replaces)
+    nq_tr = nq if bits <= 128 else min(nq, 256)
+    tr = torch.empty((nq_tr, 5), dtype=torch.int64, device=dev)
+    idx.knn_search_device(queries.data_ptr(), nq_tr, kk, ids.data_ptr(), dists.data_ptr(), tr.data_ptr(),
                           stream=stream.cuda_stream, partition=partition)
     torch.cuda.synchronize(dev)
     t = tr.cpu().numpy()
     lookups, cands, uniq, radius = (t[:, 0].astype(np.float64), t[:, 1].astype(np.float64),
                                     t[:, 2].astype(np.float64), t[:, 4].astype(np.float64))
-    alg_bytes = float((8 * lookups + 4 * cands + (bits / 8) * uniq).sum())
-    popc64 = float(uniq.sum() * W)
+    alg_bytes = float((8 * lookups + 4 * cands + (bits / 8) * uniq).sum()) * nq / nq_tr
+    popc64 = float(uniq.sum() * W) * nq / nq_tr
 
     # ---- e2e through the host-pointer C ABI ----
     hq = torch.from_numpy(np.ascontiguousarray(queries.cpu().numpy())).pin_memory()
@@ -430,7 +556,8 @@ def main():
             hd.copy_(out_d, non_blocking=True)
             torch.cuda.synchronize(dev)
 
-    e2e_step()
+    for _ in range(max(args.warmup, 3)):
+        e2e_step()
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -507,27 +634,28 @@ def main():
                     "mean_trace": {"lookups": float(lookups.mean()), "candidates": float(cands.mean()),
                                    "unique": float(uniq.mean()), "final_radius": float(radius.mean())}}
 
-    # ---- CPU baseline (rank 0, N = 1 only) ----
-    cpu = None
+    # ---- CPU baseline + parity against the reference itself (rank 0, N = 1 only) ----
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            import oracle
+        import oracle
 
-            if oracle.have_ref():
-                sample = args.cpu_sample or 64
+        if oracle.have_ref():
+            qh = queries.cpu().numpy().view(np.uint64)
+            if cfg["data"] == "uniform":
+                db_host = None  # the reference generates it (gen_uniform, io.hpp:266-277)
+            else:
                 db_host = make_codes_device(cfg, 0, cfg["n"], cfg["db_seed"], torch, dev, L).cpu().numpy().view(np.uint64)
                 torch.cuda.empty_cache()
-                qh = queries.cpu().numpy().view(np.uint64)
-                qps, threads, build_cpu_s, _ = cpu_reference_run(cfg, db_host, qh, 2, 1, sample)
-                del db_host
-                cpu = {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
-                       "sample": f"{sample} queries per step x 2 steps, full n={cfg['n']} reference "
-                                 f"index (oracle/_ref, MihIndex::knn_search, {threads} threads); "
-                                 f"reference index build {build_cpu_s:.0f}s excluded"}
-            else:
-                cpu = {"value": None, "unavailable": "oracle/_ref not built"}
-        except Exception as e:  # the baseline must not sink the GPU measurement
-            cpu = {"value": None, "error": repr(e)[:300]}
+            leg = reference_leg(cfg, args.config, qh, db_host, mih_sample=args.cpu_sample or None,
+                                log=lambda msg: print(msg, file=sys.stderr))
+            del db_host
+            cpu = reference_baseline_json(leg, args.config)
+            parity = parity_check(leg, res_ids.cpu().numpy(), res_d.cpu().numpy(), t)
+            if parity["mismatches"]:
+                print(json.dumps({"error": "parity failed: GPU rows differ from the reference", "parity": parity}))
+                sys.exit(3)
+        else:
+            cpu = {"value": None, "unavailable": "oracle/_ref not built"}
 
     if rank == 0:
         line = {
@@ -537,7 +665,8 @@ def main():
             "data": "synthetic", "config": config_desc(cfg, args, world),
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(nq * W * 8),
                     "d2h_bytes_per_step": int(nq * k * 8)},
-            "gpu_launches": launches, "verified_vs_scan": verified, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": launches, "verified_vs_scan": verified, "parity": parity, "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": clk,
             "setup": {"gen_s": gen_s, "index_build_s": build_s, "index_device_bytes": idx.device_bytes()},
         }
         print(json.dumps(line))

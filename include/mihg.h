@@ -166,6 +166,8 @@ typedef struct mihg_partition {
   mihg_allreduce_fn allreduce;
   void* user;
   uint32_t id_shards; /* 0: probe-space partition of a replicated index; 1: id-range shards */
+  uint32_t k_stop;    /* k of the GLOBAL stopping rule (id_shards: the caller's k, which may exceed
+                         a small shard's local k); 0 -> the call's k. Must be equal on all ranks. */
 } mihg_partition;
 int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
                                uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces,

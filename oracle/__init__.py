@@ -181,6 +181,17 @@ class Ref(_Lib):
         L.ref_write_codes.argtypes = [_u64p, C.c_uint64, C.c_uint32, C.c_char_p]
         L.ref_write_index.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_read_index.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.ref_knn_timed.argtypes = [C.c_void_p, _u64p, C.c_uint64, C.c_uint32, _u32p, _u32p, _u64p, C.c_int,
+                                    C.POINTER(C.c_double)]
+        L.ref_index_scan_knn_timed.argtypes = [C.c_void_p, _u64p, C.c_uint64, C.c_uint32, _u32p, _u32p,
+                                               C.c_int, C.POINTER(C.c_double)]
+        L.ref_db_new.argtypes = [_u64p, C.c_uint64, C.c_uint32, C.POINTER(C.c_void_p)]
+        L.ref_db_gen_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.ref_db_words.argtypes = [C.c_void_p]
+        L.ref_db_words.restype = C.c_void_p
+        L.ref_db_free.argtypes = [C.c_void_p]
+        L.ref_db_scan_knn_timed.argtypes = [C.c_void_p, _u64p, C.c_uint64, C.c_uint32, _u32p, _u32p, C.c_int,
+                                            C.POINTER(C.c_double)]
 
     def gen_uniform(self, n, bits, seed):
         out = np.zeros(max(n * wpc(bits), 1), np.uint64)
@@ -220,6 +231,18 @@ class Ref(_Lib):
                                           _p32(dists), threads or self.threads))
         return ids[: nq * k].reshape(nq, k), dists[: nq * k].reshape(nq, k)
 
+    def db_new(self, codes, bits):
+        codes = np.ascontiguousarray(codes, np.uint64).reshape(-1)
+        n = codes.size // wpc(bits)
+        h = C.c_void_p()
+        self._check(self.lib.ref_db_new(_p64(codes), n, bits, C.byref(h)))
+        return RefDb(self, h, bits, n)
+
+    def db_gen_uniform(self, n, bits, seed):
+        h = C.c_void_p()
+        self._check(self.lib.ref_db_gen_uniform(n, bits, seed, C.byref(h)))
+        return RefDb(self, h, bits, n)
+
     def scan_range(self, codes, bits, q, r):
         codes = np.ascontiguousarray(codes, np.uint64).reshape(-1)
         q = np.ascontiguousarray(q, np.uint64).reshape(-1)
@@ -230,6 +253,43 @@ class Ref(_Lib):
         self._check(self.lib.ref_scan_range(_p64(codes), n, bits, _p64(q), r, _p32(ids), _p32(dists),
                                             n, C.byref(cnt)))
         return ids[: cnt.value], dists[: cnt.value]
+
+
+def _pd(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class RefDb:
+    """A reference CodeDatabase held in the driver (scan-only baseline, e.g. config 5)."""
+
+    def __init__(self, owner, h, bits, n):
+        self.owner, self.h, self.bits, self.n = owner, h, bits, n
+
+    def __del__(self):
+        try:
+            self.owner.lib.ref_db_free(self.h)
+        except Exception:
+            pass
+
+    def words(self):
+        """numpy view [n, W] of the held codes (valid while this object lives)."""
+        W = wpc(self.bits)
+        p = self.owner.lib.ref_db_words(self.h)
+        buf = (C.c_uint64 * (self.n * W)).from_address(p)
+        return np.frombuffer(buf, np.uint64).reshape(self.n, W)
+
+    def scan_knn_timed(self, queries, k, threads=None):
+        return _scan_timed(self.owner, self.owner.lib.ref_db_scan_knn_timed, self.h, self.bits, queries, k, threads)
+
+
+def _scan_timed(owner, fn, h, bits, queries, k, threads):
+    queries = np.ascontiguousarray(queries, np.uint64).reshape(-1)
+    nq = queries.size // wpc(bits)
+    ids = np.zeros(max(nq * k, 1), np.uint32)
+    dists = np.zeros(max(nq * k, 1), np.uint32)
+    secs = np.zeros(max(nq, 1), np.float64)
+    owner._check(fn(h, _p64(queries), nq, k, _p32(ids), _p32(dists), threads or owner.threads, _pd(secs)))
+    return ids[: nq * k].reshape(nq, k), dists[: nq * k].reshape(nq, k), secs[:nq]
 
 
 class _Handle:
@@ -259,6 +319,24 @@ class _Handle:
             rc = L.or_knn(self.h, _p64(queries), nq, k, _p32(ids), _p32(dists), _p64(tr))
         self.owner._check(rc)
         return ids[: nq * k].reshape(nq, k), dists[: nq * k].reshape(nq, k), tr[: nq * 5].reshape(nq, 5)
+
+    def knn_timed(self, queries, k, threads=None):
+        """ref_knn plus the wall time of every query (seconds): (ids, dists, traces, secs)."""
+        queries = np.ascontiguousarray(queries, np.uint64).reshape(-1)
+        nq = queries.size // wpc(self.bits)
+        ids = np.zeros(max(nq * k, 1), np.uint32)
+        dists = np.zeros(max(nq * k, 1), np.uint32)
+        tr = np.zeros(max(nq * 5, 1), np.uint64)
+        secs = np.zeros(max(nq, 1), np.float64)
+        self.owner._check(self.owner.lib.ref_knn_timed(self.h, _p64(queries), nq, k, _p32(ids), _p32(dists),
+                                                       _p64(tr), threads or self.owner.threads, _pd(secs)))
+        return (ids[: nq * k].reshape(nq, k), dists[: nq * k].reshape(nq, k), tr[: nq * 5].reshape(nq, 5),
+                secs[:nq])
+
+    def scan_knn_timed(self, queries, k, threads=None):
+        """the reference's scan_knn over this index's own database: (ids, dists, secs)."""
+        return _scan_timed(self.owner, self.owner.lib.ref_index_scan_knn_timed, self.h, self.bits, queries, k,
+                           threads)
 
     def range(self, q, r):
         q = np.ascontiguousarray(q, np.uint64).reshape(-1)

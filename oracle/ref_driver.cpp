@@ -11,6 +11,7 @@
 // mih.hpp / costmodel.hpp are deliberately NOT included: they pull in <gmpxx.h>, which is
 // absent. Every entry point catches C++ exceptions and maps them to
 // integer codes (1 = std::invalid_argument, 2 = FormatError/other, 3 = bad_alloc).
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -218,6 +219,75 @@ int ref_knn(void* h, const uint64_t* queries, uint64_t nq, uint32_t k, uint32_t*
       }
       if (traces) put_trace(tr, traces + qi * 5);
     });
+  });
+}
+
+// ref_knn with the wall time of every query (seconds, measured inside its thread): the
+// per-query statistics of tools/mih.cpp:198-213 / :316-339. secs: nq doubles or NULL.
+int ref_knn_timed(void* h, const uint64_t* queries, uint64_t nq, uint32_t k, uint32_t* ids,
+                  uint32_t* dists, uint64_t* traces, int nthreads, double* secs) {
+  return guarded([&] {
+    const mih::MihIndex& idx = *static_cast<mih::MihIndex*>(h);
+    const uint32_t bits = idx.db().bits(), wpc = mih::words_per_code(bits);
+    std::vector<mih::SearchScratch> scratch(nthreads > 0 ? nthreads : 1);
+    parallel_for(nq, nthreads, [&](uint64_t qi, int t) {
+      mih::SearchTrace tr;
+      const auto t0 = std::chrono::steady_clock::now();
+      mih::Neighbors res = idx.knn_search({queries + qi * wpc, bits}, k, &tr, &scratch[t]);
+      if (secs) secs[qi] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      for (uint32_t i = 0; i < res.size(); ++i) {
+        ids[qi * k + i] = res[i].id;
+        dists[qi * k + i] = res[i].dist;
+      }
+      if (traces) put_trace(tr, traces + qi * 5);
+    });
+  });
+}
+
+namespace {
+void scan_timed(const mih::CodeDatabase& db, const uint64_t* queries, uint64_t nq, uint32_t k,
+                uint32_t* ids, uint32_t* dists, int nthreads, double* secs) {
+  const uint32_t bits = db.bits(), wpc = mih::words_per_code(bits);
+  parallel_for(nq, nthreads, [&](uint64_t qi, int) {
+    const auto t0 = std::chrono::steady_clock::now();
+    mih::Neighbors res = mih::scan_knn(db, {queries + qi * wpc, bits}, k);
+    if (secs) secs[qi] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (uint32_t i = 0; i < res.size(); ++i) {
+      ids[qi * k + i] = res[i].id;
+      dists[qi * k + i] = res[i].dist;
+    }
+  });
+}
+}  // namespace
+
+// scan_knn (scan.hpp:43-68) over an index's own database (MihIndex::db(), index.hpp:143): the
+// reference's linear-scan baseline beside its MIH on the same codes, no second copy.
+int ref_index_scan_knn_timed(void* h, const uint64_t* queries, uint64_t nq, uint32_t k, uint32_t* ids,
+                             uint32_t* dists, int nthreads, double* secs) {
+  return guarded([&] {
+    scan_timed(static_cast<mih::MihIndex*>(h)->db(), queries, nq, k, ids, dists, nthreads, secs);
+  });
+}
+
+// A CodeDatabase held by the driver (configs whose reference index does not fit host memory:
+// only scan_knn runs over it).
+int ref_db_new(const uint64_t* codes, uint64_t n, uint32_t bits, void** out) {
+  return guarded([&] { *out = new mih::CodeDatabase(make_db(codes, n, bits)); });
+}
+
+// gen_uniform (io.hpp:266-277) straight into a held CodeDatabase.
+int ref_db_gen_uniform(uint64_t n, uint32_t bits, uint64_t seed, void** out) {
+  return guarded([&] { *out = new mih::CodeDatabase(mih::gen_uniform(n, bits, seed)); });
+}
+
+const uint64_t* ref_db_words(void* h) { return static_cast<mih::CodeDatabase*>(h)->raw_words().data(); }
+
+void ref_db_free(void* h) { delete static_cast<mih::CodeDatabase*>(h); }
+
+int ref_db_scan_knn_timed(void* h, const uint64_t* queries, uint64_t nq, uint32_t k, uint32_t* ids,
+                          uint32_t* dists, int nthreads, double* secs) {
+  return guarded([&] {
+    scan_timed(*static_cast<mih::CodeDatabase*>(h), queries, nq, k, ids, dists, nthreads, secs);
   });
 }
 

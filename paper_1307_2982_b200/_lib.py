@@ -59,7 +59,7 @@ class Partition(C.Structure):
     """mihg_partition: probe-space partition of a multi-GPU kNN call."""
 
     _fields_ = [("count", C.c_uint32), ("rank", C.c_uint32), ("allreduce", ALLREDUCE_FN),
-                ("user", C.c_void_p), ("id_shards", C.c_uint32)]
+                ("user", C.c_void_p), ("id_shards", C.c_uint32), ("k_stop", C.c_uint32)]
 
 
 class Profile(C.Structure):

@@ -301,6 +301,7 @@ int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint6
       pt.allreduce = part->allreduce;
       pt.user = part->user;
       pt.id_shards = part->id_shards != 0;
+      pt.k_stop = part->k_stop;
     }
     mihg::KnnOptions opt;
     opt.part = part ? &pt : nullptr;
@@ -319,17 +320,18 @@ int mihg_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32
     DeviceGuard g(ix.device);
     std::lock_guard<std::mutex> lk(ix.mu);
     cudaStream_t st = ix.stream;
-    mihg::DeviceBuffer<uint64_t> dq(nq * ix.W, st);
-    mihg::DeviceBuffer<uint32_t> di(std::max<uint64_t>(nq * k, 1), st), dd(std::max<uint64_t>(nq * k, 1), st);
-    mihg::DeviceBuffer<mihg::Trace> dt(traces ? nq : 0, st);
-    MIHG_CUDA(cudaMemcpyAsync(dq.get(), queries, nq * ix.W * 8, cudaMemcpyHostToDevice, st));
-    mihg::knn_device(ix, dq.get(), nq, k, di.get(), dd.get(), traces ? dt.get() : nullptr, st);
+    uint64_t* dq = mihg::Index::grow(ix.stage_q, nq * ix.W, st);
+    uint32_t* di = mihg::Index::grow(ix.stage_ids, std::max<uint64_t>(nq * k, 1), st);
+    uint32_t* dd = mihg::Index::grow(ix.stage_dists, std::max<uint64_t>(nq * k, 1), st);
+    mihg::Trace* dt = traces ? reinterpret_cast<mihg::Trace*>(mihg::Index::grow(ix.stage_tr, nq * sizeof(mihg::Trace), st))
+                             : nullptr;
+    MIHG_CUDA(cudaMemcpyAsync(dq, queries, nq * ix.W * 8, cudaMemcpyHostToDevice, st));
+    mihg::knn_device(ix, dq, nq, k, di, dd, dt, st);
     if (k) {
-      MIHG_CUDA(cudaMemcpyAsync(out_ids, di.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
-      MIHG_CUDA(cudaMemcpyAsync(out_dists, dd.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
+      MIHG_CUDA(cudaMemcpyAsync(out_ids, di, nq * k * 4, cudaMemcpyDeviceToHost, st));
+      MIHG_CUDA(cudaMemcpyAsync(out_dists, dd, nq * k * 4, cudaMemcpyDeviceToHost, st));
     }
-    if (traces)
-      MIHG_CUDA(cudaMemcpyAsync(traces, dt.get(), nq * sizeof(mihg::Trace), cudaMemcpyDeviceToHost, st));
+    if (traces) MIHG_CUDA(cudaMemcpyAsync(traces, dt, nq * sizeof(mihg::Trace), cudaMemcpyDeviceToHost, st));
     MIHG_CUDA(cudaStreamSynchronize(st));
   });
 }
@@ -367,13 +369,13 @@ int mihg_scan_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, u
     DeviceGuard g(ix.device);
     std::lock_guard<std::mutex> lk(ix.mu);
     cudaStream_t st = ix.stream;
-    mihg::DeviceBuffer<uint64_t> dq(nq * ix.W, st);
-    mihg::DeviceBuffer<uint32_t> di(nq * k, st), dd(nq * k, st);
-    MIHG_CUDA(cudaMemcpyAsync(dq.get(), queries, nq * ix.W * 8, cudaMemcpyHostToDevice, st));
-    mihg::scan_knn_device(ix.codes.get(), ix.n, ix.bits, ix.id_base, dq.get(), nq, k, di.get(),
-                          dd.get(), st);
-    MIHG_CUDA(cudaMemcpyAsync(out_ids, di.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
-    MIHG_CUDA(cudaMemcpyAsync(out_dists, dd.get(), nq * k * 4, cudaMemcpyDeviceToHost, st));
+    uint64_t* dq = mihg::Index::grow(ix.stage_q, nq * ix.W, st);
+    uint32_t* di = mihg::Index::grow(ix.stage_ids, nq * k, st);
+    uint32_t* dd = mihg::Index::grow(ix.stage_dists, nq * k, st);
+    MIHG_CUDA(cudaMemcpyAsync(dq, queries, nq * ix.W * 8, cudaMemcpyHostToDevice, st));
+    mihg::scan_knn_device(ix.codes.get(), ix.n, ix.bits, ix.id_base, dq, nq, k, di, dd, st);
+    MIHG_CUDA(cudaMemcpyAsync(out_ids, di, nq * k * 4, cudaMemcpyDeviceToHost, st));
+    MIHG_CUDA(cudaMemcpyAsync(out_dists, dd, nq * k * 4, cudaMemcpyDeviceToHost, st));
     MIHG_CUDA(cudaStreamSynchronize(st));
   });
 }

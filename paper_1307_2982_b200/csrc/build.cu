@@ -115,6 +115,22 @@ __global__ void extract_keys_kernel(const uint64_t* __restrict__ codes, uint32_t
   }
 }
 
+// Loaded tables: entry i of table j must hold an id seen exactly once whose substring key is
+// keys[i] (bit 0 of *bad: key mismatch, bit 1: repeated id).
+__global__ void verify_pre_kernel(const uint64_t* __restrict__ codes, uint32_t W, uint64_t n,
+                                  DevSubstring sub, const uint32_t* __restrict__ positions,
+                                  const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ids,
+                                  uint32_t* __restrict__ seen, uint32_t* __restrict__ bad) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t id = ids[i];
+    uint32_t f = 0;
+    if (extract_key(codes + uint64_t(id) * W, sub, positions) != keys[i]) f |= 1;
+    if (atomicOr(seen + (id >> 5), 1u << (id & 31)) & (1u << (id & 31))) f |= 2;
+    if (f) atomicOr(bad, f);
+  }
+}
+
 __global__ void extract_all_keys_kernel(const uint64_t* __restrict__ codes, uint32_t W,
                                         uint64_t count, uint32_t m, const DevSubstring* __restrict__ subs,
                                         const uint32_t* __restrict__ positions, uint32_t* __restrict__ keys) {
@@ -273,6 +289,20 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
   if (n && opt.pre) {  // tables from an index file: already in (key, id) order
     MIHG_CUDA(cudaMemcpyAsync(keys.get(), (*opt.pre)[j].keys.data(), n * 4, cudaMemcpyHostToDevice, st));
     MIHG_CUDA(cudaMemcpyAsync(t->ids.get(), (*opt.pre)[j].ids.data(), n * 4, cudaMemcpyHostToDevice, st));
+    // ids < n was checked by the loader
+    DeviceBuffer<uint32_t> seen((n + 31) / 32 + 1, st);
+    MIHG_CUDA(cudaMemsetAsync(seen.get(), 0, ((n + 31) / 32 + 1) * 4, st));
+    uint32_t* bad = seen.get() + (n + 31) / 32;
+    verify_pre_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx.codes.get(), idx.W, n, idx.subs[j],
+                                                        idx.d_positions.get(), keys.get(), t->ids.get(),
+                                                        seen.get(), bad);
+    MIHG_LAUNCH();
+    uint32_t hbad = 0;
+    MIHG_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
+    MIHG_CUDA(cudaStreamSynchronize(st));
+    if (hbad & 2) throw InconsistentTable(j, "table " + std::to_string(j) + " lists an id more than once");
+    if (hbad & 1)
+      throw InconsistentTable(j, "table " + std::to_string(j) + " files an id under a key other than its substring");
   } else if (n) {
     extract_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx.codes.get(), idx.W, n, idx.subs[j],
                                                           idx.d_positions.get(), keys.get(),

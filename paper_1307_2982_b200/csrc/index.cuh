@@ -50,7 +50,15 @@ struct BuildOptions {
   // Sparse tables: 1-bit-per-bucket occupancy bitmap in front of the directory, so a probe of
   // an empty bucket is one 4-byte (L2-resident per key slice) read instead of a DRAM sector.
   bool occupancy = false;
-  const std::vector<PreTable>* pre = nullptr;  // use these tables instead of sorting  // measured: config 4 703K -> 674K q/s with it (dependent L2 read)
+  // measured: occupancy on, config 4 703K -> 674K q/s (a dependent L2 read per probe)
+  const std::vector<PreTable>* pre = nullptr;  // use these tables instead of sorting
+};
+
+// A loaded table (BuildOptions::pre) whose entries are not a permutation of [0, n) filed under
+// their own substring key: the stateless first-discovery dedup of the kNN kernels relies on it.
+struct InconsistentTable : std::runtime_error {
+  uint32_t table;
+  InconsistentTable(uint32_t j, const std::string& what) : std::runtime_error(what), table(j) {}
 };
 
 struct Index {
@@ -70,6 +78,16 @@ struct Index {
   DeviceBuffer<DevTable> d_tables;
   std::mutex mu;  // one host call at a time per index (workspace is shared)
   struct Workspace* ws = nullptr;
+  // grow-only device staging of the host-pointer entry points (queries in, results out), reused
+  // across calls so a host call allocates nothing once warm
+  DeviceBuffer<uint64_t> stage_q;
+  DeviceBuffer<uint32_t> stage_ids, stage_dists;
+  DeviceBuffer<unsigned char> stage_tr;
+  template <typename T>
+  static T* grow(DeviceBuffer<T>& b, uint64_t n, cudaStream_t st) {
+    if (b.size() < n) b = DeviceBuffer<T>(n, st);
+    return b.get();
+  }
   ~Index();
 };
 

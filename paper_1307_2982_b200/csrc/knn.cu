@@ -66,6 +66,10 @@ Index::~Index() {
   if (stream) cudaStreamSynchronize(stream);
   delete ws;
   ws = nullptr;
+  stage_q.reset();
+  stage_ids.reset();
+  stage_dists.reset();
+  stage_tr.reset();
   codes.reset();
   d_positions.reset();
   d_subs.reset();
@@ -1006,6 +1010,10 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
 
   ProbeArgs p = make_probe_args(idx, ws, d_q);
   uint64_t part_lo = 0, part_hi = idx.n;  // id range this rank scans if queries switch to K6
+  // the stopping rule's k: the caller's global k when shards hold fewer than k codes (id_shards)
+  const uint32_t kstop = part && part->k_stop ? part->k_stop : k;
+  if (part && part->k_stop && part->k_stop < k) throw InvalidArgument("partitioned knn: k_stop below k");
+  bool hybrid_ok = true;  // the scan switch must be the same decision on every rank
   if (part && part->id_shards) {  // every shard probes every ring; only the counts are global
     if (part->rank >= part->count) throw InvalidArgument("partitioned knn: rank must be < count");
     if (ws.hist_g.size() < nq * b1) ws.hist_g = DeviceBuffer<uint32_t>(ws.nq_cap * b1, st);
@@ -1022,6 +1030,9 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     const uint64_t per = (idx.n + part->count - 1) / part->count;
     part_lo = std::min<uint64_t>(idx.n, uint64_t(part->rank) * per);
     part_hi = std::min<uint64_t>(idx.n, part_lo + per);
+    // the last rank's range is the smallest; every rank evaluates the same condition
+    const uint64_t last_lo = std::min<uint64_t>(idx.n, uint64_t(part->count - 1) * per);
+    hybrid_ok = idx.n - last_lo >= k;
   }
 
   std::vector<uint64_t> lookups_prefix;
@@ -1029,8 +1040,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   uint32_t* act_out = ws.act1.get();
   uint64_t nact = nq;
   uint64_t acc = 0;
-  const double alpha =
-      (d_tr || (part && (part->id_shards || part_hi - part_lo < k))) ? 0.0 : hybrid_alpha();
+  const double alpha = (d_tr || (part && part->id_shards) || !hybrid_ok) ? 0.0 : hybrid_alpha();
   const double scan_pairs = double(idx.n) * scan_cost_per_code(idx.bits),
                probe_pairs = 36.0 + 15.0 * (idx.W - 1);
   uint32_t* switched = nullptr;
@@ -1077,7 +1087,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
     const unsigned g = unsigned((nact * 32 + 255) / 256);
     mih_round_end_kernel<<<g, 256, 0, st>>>(act_in, uint32_t(nact), act_out, ws.counters.get(),
-                                             hist_end, b1, ws.ubound.get(), k, r,
+                                             hist_end, b1, ws.ubound.get(), kstop, r,
                                              ws.final_r.get(), ws.bufcnt.get(), ws.buf.get(), cap);
     MIHG_LAUNCH();
     nact = read_counter(ws.counters.get(), ws.h_counter, st);  // synchronizes the stream

@@ -20,6 +20,7 @@ struct Partition {
   int (*allreduce)(void* user, void* dev_ptr, uint64_t count, int dtype, void* stream) = nullptr;
   void* user = nullptr;
   bool id_shards = false;  // id-range shards with global stopping (no probe split)
+  uint32_t k_stop = 0;     // k of the global stopping rule (0: the call's k)
 };
 
 struct KnnOptions {

@@ -164,13 +164,14 @@ Index* read_index(const std::string& path, int device, const BuildOptions& base_
   }
   // tables (io.hpp:390-418 + SubstringTable::from_groups, table.hpp:224-270)
   std::vector<PreTable> pre(m);
+  std::vector<uint64_t> table_at(m);
   for (uint32_t j = 0; j < m; ++j) {
-    const uint64_t table_at = r.off;
+    table_at[j] = r.off;
     const uint32_t s = r.get<uint32_t>("table width");
     const uint64_t entries = r.get<uint64_t>("table entry count");
     const uint64_t groups = r.get<uint64_t>("table group count");
     auto invalid = [&](const std::string& what) {
-      return FormatError("invalid table " + std::to_string(j) + ": " + what, table_at);
+      return FormatError("invalid table " + std::to_string(j) + ": " + what, table_at[j]);
     };
     if (s == 0 || s > kMaxTableBits)
       throw invalid("SubstringTable: key width must be in [1, 32], got " + std::to_string(s));
@@ -199,6 +200,9 @@ Index* read_index(const std::string& path, int device, const BuildOptions& base_
       if (arena > (uint64_t(1) << 32)) throw invalid("table arena exceeds 2^32 slots");
       uint32_t mm = mask;
       t.keys.resize(at + e);
+      // buckets past 2^s (possible when s < 5) are unreachable by any probe: a table holding
+      // entries there is rejected (the reference keeps them, dead; the GPU directory has no slot)
+      if (s < 5 && (uint64_t(mask) >> (uint64_t(1) << s)) != 0) throw invalid("table group mask has buckets >= 2^s");
       for (uint32_t i = 0; i < c; ++i) {  // bucket i of the group = i-th set bit of the mask
         const uint32_t bit = uint32_t(__builtin_ctz(mm));
         mm &= mm - 1;
@@ -227,7 +231,11 @@ Index* read_index(const std::string& path, int device, const BuildOptions& base_
                       r.off);
   BuildOptions opt = base_opt;
   opt.pre = &pre;
-  return build_index(codes.data(), false, n, bits, m, lengths.data(), positions.data(), device, 0, opt);
+  try {
+    return build_index(codes.data(), false, n, bits, m, lengths.data(), positions.data(), device, 0, opt);
+  } catch (const InconsistentTable& e) {
+    throw FormatError(std::string("inconsistent index: ") + e.what(), table_at[e.table]);
+  }
 }
 
 }  // namespace mihg

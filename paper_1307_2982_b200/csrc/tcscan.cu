@@ -11,17 +11,17 @@
 // items; consecutive items of one query tile form a segment (one id range, one set of lists).
 // 22 warps, warp-specialised:
 //   warps 0-15  epilogue: thread (warp % 4, lane) owns query row 32 (warp % 4) + lane; group
-//               g = warp / 4 drains columns [32 g, 32 g + 32) of every 128-code tile and keeps its
+//               g = warp / 4 drains columns [64 g, 64 g + 64) of every 256-code tile and keeps its
 //               own candidate list per query (id order, compacted to the exact top-k when it reaches
 //               2k entries; scanlist.cuh, as in K6), under a bound shared by all lists of the query.
-//   warps 16-19 producers: each thread takes one code per tile from the raw ring and expands it
+//   warps 16-19 producers: each thread takes two codes per tile from the raw ring and expands them
 //               to K bytes of 0/1 in the 128-byte-swizzled K-major layout of the B operand.
 //   warp 20     TMEM allocation and the single-thread tcgen05.mma issue.
 //   warp 21     loader: one thread keeps kRaw raw code tiles in flight from HBM/L2 into shared
 //               memory with 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx).
 // Pipelines: B stages full/empty (producers <-> MMA, mbarriers; tcgen05.commit frees a stage) and
-// four TMEM accumulators of 128 columns (MMA <-> epilogue), so the MMA runs up to four tiles
-// ahead of the accumulator drain.
+// two TMEM accumulators of 256 columns (MMA <-> epilogue), so the MMA runs one tile ahead of the
+// accumulator drain. The query tile (A operand) sits in shared memory in B's layout.
 // The per-query selection over the lists is K6's (gather + select_topk), so ties resolve to the
 // smaller id exactly as scan.hpp:24-26.
 #include <algorithm>
@@ -39,8 +39,6 @@ namespace {
 constexpr int kTcM = 128;        // queries per CTA (TMEM lanes)
 constexpr int kTcN = 256;        // codes per tile (MMA N)
 constexpr int kAcc = 2;          // TMEM accumulators of kTcN columns (all 512 columns)
-constexpr uint32_t kATmemCol = kAcc * kTcN;
-constexpr uint32_t kSfaCol = 448, kSfbCol = 480;  // E8M0 block scales of the E2M1 variant
 constexpr int kEpiGroups = 4;    // epilogue groups of 4 warps; group g drains columns [32 g, 32 g + 32)
 constexpr int kEpiCols = kTcN / kEpiGroups;
 constexpr int kEpiWarps = 4 * kEpiGroups;
@@ -67,9 +65,11 @@ struct TcArgs {
   uint32_t slots;
   int32_t* dump;     // debug: nq x n distances (tests only), or nullptr
   uint32_t* gbound;  // [q]: smallest k-th distance proven by any list of the query (0xFFFFFFFF = none)
-  unsigned long long* prof;  // debug (MIHG_TC_PROF=1): [32 warps][8] cycle counters summed over CTAs
-  uint32_t mma_only;         // timing probe (MIHG_TC_MMA_ONLY=1|2): only the MMA stream runs (2: rotating
-                             // B stages); results are NOT produced — measures the tensor ceiling
+#ifdef MIHG_TC_DEBUG
+  unsigned long long* prof;  // debug build only: [32 warps][8] cycle counters summed over CTAs
+  uint32_t mma_only;         // debug build only: only the MMA stream runs (2: rotating B stages);
+                             // results are NOT produced — measures the tensor ceiling
+#endif
 };
 
 // ---- PTX wrappers (tcgen05 / mbarrier) ----
@@ -119,52 +119,6 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// D[tmem] (+)= A[tmem] . B[smem]^T, kind::i8 (A signed in TMEM, B unsigned in shared memory)
-__device__ __forceinline__ void tc_mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// D[tmem] (+)= A[tmem] . B[smem]^T, kind::mxf4 (E2M1, f32 accumulate), unit E8M0 block scales in TMEM
-__device__ __forceinline__ void tc_mma_f4_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accumulate, uint32_t tmem_sfa, uint32_t tmem_sfb) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n\t}" ::"r"(
-          tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
-      : "memory");
-}
-constexpr uint32_t tc_idesc_f4(uint32_t M, uint32_t N) {
-  return (1u << 7) | (1u << 10) | ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24);
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-               : "memory");
-}
-// 8 bits -> 8 nibbles (bit i -> bit 4 i), by shift-or-mask steps (a multiply would carry)
-__device__ __forceinline__ uint32_t spread_n8(uint32_t x) {
-  x = (x | (x << 12)) & 0x000F000Fu;
-  x = (x | (x << 6)) & 0x03030303u;
-  return (x | (x << 3)) & 0x11111111u;
-}
-
-// 32 TMEM lanes x 16 consecutive 32-bit columns <- 16 registers per thread (lane = thread).
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-}
-
 // Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 bytes in 1024-byte
 // atoms of 8 rows (SBO = 1024), the 16-byte chunk c of row r stored at c ^ (r mod 8); a K extent
 // above 128 bytes continues in the next 128-byte K block (a separate rows x 128 B region).
@@ -219,10 +173,10 @@ __device__ __forceinline__ void raw_span(const uint64_t* codes, uint64_t id0, ui
   bytes = e16 > s16 ? uint32_t(e16 - s16) : 0u;
 }
 
-template <int KB, bool kF4 = false>
+template <int KB>
 struct TcCfg {
   static constexpr int W = KB / 64;
-  static constexpr uint32_t kOpBytes = kF4 ? KB / 2 : KB;
+  static constexpr uint32_t kOpBytes = KB;
   static constexpr int kSteps = kOpBytes / 32;
   static constexpr uint32_t kKBp = (kOpBytes + 127) / 128 * 128;  // whole 128-byte swizzle rows
   static constexpr uint32_t kA = kTcM * kKBp;  // A (queries) in shared memory
@@ -232,9 +186,9 @@ struct TcCfg {
   static constexpr uint32_t kSmem = 1024 + kA + kStages * kB + kRaw * kRawBytes;  // + barriers/hist
 };
 
-template <int KB, bool kDump, bool kF4>
+template <int KB, bool kDump>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
-  using Cfg = TcCfg<KB, kF4>;
+  using Cfg = TcCfg<KB>;
   constexpr int W = Cfg::W;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -253,6 +207,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   uint32_t* hist_all = tmem_slot + 4;  // kEpiWarps * (bits + 1)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef MIHG_TC_DEBUG
   unsigned long long wcyc[4] = {0, 0, 0, 0};
   auto wait_k = [&](uint64_t* bar, uint32_t parity, int kind) {
     const unsigned long long c0 = a.prof ? clock64() : 0;
@@ -260,6 +215,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     if (a.prof) wcyc[kind] += clock64() - c0;
   };
   const unsigned long long t_start = clock64();
+#else
+  auto wait_k = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
+#endif
 
   if (warp == kMmaWarp) {
     if (lane == 0) {
@@ -285,24 +243,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if constexpr (kF4) {
-    if (warp < 4) {
-      uint32_t ones[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) ones[i] = 0x7F7F7F7Fu;
-      tmem_st8(tmem + ((warp * 32) << 16) + kSfaCol, ones);
-      tmem_st8(tmem + ((warp * 32) << 16) + kSfbCol, ones);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-  }
 
   // This CTA's work items [i0, i1) (tile-major): consecutive items of one query tile form a
   // segment over one contiguous id range, with one candidate list per (query, group).
   const uint64_t items = uint64_t(a.qtiles) * a.nch;
   const uint64_t i0 = uint64_t(blockIdx.x) * a.ipc, i1 = min(items, i0 + a.ipc);
   uint32_t tg = 0;  // tiles processed by this CTA so far: drives every pipeline phase
+#ifdef MIHG_TC_DEBUG
   uint32_t mo_phase = 0;  // mma_only probe
   uint32_t tiles_total = 0;
+#endif
   for (uint64_t it = i0; it < i1;) {
     const uint32_t Q = uint32_t(it / a.nch);
     const uint64_t it_end = min(i1, uint64_t(Q + 1) * a.nch);
@@ -313,22 +263,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     const uint64_t q0 = uint64_t(Q) * kTcM;
     it = it_end;
 
-    // A operand in TMEM (columns kATmemCol..): lane r = query q0 + r as K bytes of +1 (bit 0) /
-    // -1 (bit 1), four per 32-bit column; padding rows zero. Written by warps 0-3 (lanes 32 w..).
+    // A operand in shared memory (128B-swizzled K-major, like B): row r = query q0 + r as K bytes
+    // of +1 (bit 0) / -1 (bit 1); padding rows zero. Written by warps 0-3 (rows 32 w..).
     if (warp < 4) {
       const uint32_t r = warp * 32 + lane;
       const uint64_t q = q0 + r;
-      if constexpr (kF4) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          uint32_t w8[8];
-          const uint64_t word = q < a.nq ? __ldg(a.queries + q * W + w) : 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            w8[i] = q < a.nq ? ((spread_n8(uint32_t(word >> (8 * i)) & 0xFFu) << 3) | 0x22222222u) : 0u;
-          tmem_st8(tmem + ((warp * 32) << 16) + kATmemCol + w * 8, w8);
-        }
-      } else
 #pragma unroll
       for (int c = 0; c < KB / 16; ++c) {  // 16-byte chunk c = query bits [16 c, 16 c + 16)
         uint4 o = make_uint4(0, 0, 0, 0);
@@ -341,16 +280,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         }
         *reinterpret_cast<uint4*>(sA + core_off<KB>(r, c, kTcM)) = o;
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
 
+#ifdef MIHG_TC_DEBUG
     if (a.mma_only) {
       if (warp == kMmaWarp && lane == 0) {
-        constexpr uint32_t idesc = kF4 ? tc_idesc_f4(kTcM, kTcN) : tc_idesc(kTcM, kTcN);
+        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
         const uint32_t b_addr = smem_u32(sB);
         for (uint32_t t = tg; t < tg + T; ++t) {
 #pragma unroll
@@ -364,10 +303,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         mo_phase ^= 1;
       }
       __syncwarp();
-    } else if (warp == kMmaWarp) {
+    } else
+#endif
+    if (warp == kMmaWarp) {
       // ===== MMA issuer =====
       if (lane == 0) {
-        constexpr uint32_t idesc = kF4 ? tc_idesc_f4(kTcM, kTcN) : tc_idesc(kTcM, kTcN);
+        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
         const uint32_t b_addr = smem_u32(sB);
         for (uint32_t t = tg; t < tg + T; ++t) {
           const uint32_t s = t % S, ph = (t / S) & 1, b = t % kAcc, bph = (t / kAcc) & 1;
@@ -489,10 +430,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         for (int sc = 0; sc < kEpiCols / 32; ++sc) {  // 32-column sub-chunks of this group's columns
         int32_t v[32];
         tmem_ld32(taddr0 + b * kTcN + sc * 32, v);
-        if constexpr (kF4 && kDump) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __float2int_rn(__int_as_float(v[j]));
-        }
         if (sc == kEpiCols / 32 - 1) {
           tc_fence_before();  // accumulator drained into registers: hand it back
           __syncwarp();
@@ -505,35 +442,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
               if (id0 + j < hi) a.dump[q * a.n + id0 + j] = v[j] + pq;
         }
         const int32_t thr = min(own, shared_b) - pq;
-        // tree minimum (independent 3-input mins, short dependency chain); the E2M1 variant's
-        // accumulators are exact small integers in f32 and are compared as floats
-        bool any_hit;
-        if constexpr (kF4 && !kDump) {
-          float m8[11];
+        // tree minimum (independent 3-input mins, short dependency chain)
+        int32_t m8[11];
 #pragma unroll
-          for (int i = 0; i < 10; ++i)
-            m8[i] = fminf(fminf(__int_as_float(v[3 * i]), __int_as_float(v[3 * i + 1])), __int_as_float(v[3 * i + 2]));
-          m8[10] = fminf(__int_as_float(v[30]), __int_as_float(v[31]));
-          const float m3a = fminf(fminf(m8[0], m8[1]), m8[2]), m3b = fminf(fminf(m8[3], m8[4]), m8[5]);
-          const float m3c = fminf(fminf(m8[6], m8[7]), m8[8]), m3d = fminf(m8[9], m8[10]);
-          any_hit = fminf(fminf(m3a, m3b), fminf(m3c, m3d)) <= float(thr);
-        } else {
-          int32_t m8[11];
-#pragma unroll
-          for (int i = 0; i < 10; ++i) m8[i] = min(min(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
-          m8[10] = min(v[30], v[31]);
-          const int32_t m3a = min(min(m8[0], m8[1]), m8[2]), m3b = min(min(m8[3], m8[4]), m8[5]);
-          const int32_t m3c = min(min(m8[6], m8[7]), m8[8]), m3d = min(m8[9], m8[10]);
-          any_hit = min(min(m3a, m3b), min(m3c, m3d)) <= thr;
-        }
+        for (int i = 0; i < 10; ++i) m8[i] = min(min(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+        m8[10] = min(v[30], v[31]);
+        const int32_t m3a = min(min(m8[0], m8[1]), m8[2]), m3b = min(min(m8[3], m8[4]), m8[5]);
+        const int32_t m3c = min(min(m8[6], m8[7]), m8[8]), m3d = min(m8[9], m8[10]);
+        const bool any_hit = min(min(m3a, m3b), min(m3c, m3d)) <= thr;
         if (any_hit) {
           // hit mask, then the (few) hits re-derive their distance from the code words (L2-hot)
           uint32_t m = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if constexpr (kF4 && !kDump) m |= uint32_t(__int_as_float(v[j]) <= float(thr)) << j;
-            else m |= uint32_t(v[j] <= thr) << j;
-          }
+          for (int j = 0; j < 32; ++j) m |= uint32_t(v[j] <= thr) << j;
           while (m) {
             const uint32_t j = __ffs(m) - 1;
             m &= m - 1;
@@ -566,52 +487,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
       if (qvalid) a.counts[q * a.slots + slot] = cnt;
     }
     tg += T;
+#ifdef MIHG_TC_DEBUG
     tiles_total += T;
+#endif
     // segment end: every MMA of the segment was drained by the epilogue, so A may be reloaded
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
   }
+#ifdef MIHG_TC_DEBUG
   if (a.prof && lane == 0) {
     unsigned long long* pr = a.prof + warp * 8;
     atomicAdd(pr + 0, clock64() - t_start);
     for (int i = 0; i < 4; ++i) atomicAdd(pr + 1 + i, wcyc[i]);
     atomicAdd(pr + 5, (unsigned long long)tiles_total);
   }
+#endif
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
-template <int KB, bool kF4>
+template <int KB>
 size_t tc_smem_bytes(uint32_t bits) {
-  using Cfg = TcCfg<KB, kF4>;
+  using Cfg = TcCfg<KB>;
   return Cfg::kSmem + (2 * Cfg::kStages + 2 * kAcc + 2 * kRaw) * 8 + 16 + size_t(kEpiWarps) * (bits + 1) * 4;
 }
 
-template <int KB, bool kDump, bool kF4>
+template <int KB, bool kDump>
 void launch_tc_k(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  const size_t smem = tc_smem_bytes<KB, kF4>(a.bits);
-  MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, kDump, kF4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = tc_smem_bytes<KB>(a.bits);
+  MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, kDump>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
-  tc_scan_kernel<KB, kDump, kF4><<<grid, kTcThreads, smem, st>>>(a);
+  tc_scan_kernel<KB, kDump><<<grid, kTcThreads, smem, st>>>(a);
   MIHG_LAUNCH();
 }
 
-// MMA kind: int8 (default) or the experimental block-scaled E2M1 (MIHG_TC_KIND=fp4).
 template <int KB>
 void launch_tc(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  // the E2M1 variant keeps A and its block scales in TMEM, which the two 256-column accumulators
-  // of this tile geometry fill completely: int8 only
-  const bool f4 = false;
-  if (a.dump) {
-    if (f4) launch_tc_k<KB, true, true>(a, grid, st);
-    else launch_tc_k<KB, true, false>(a, grid, st);
-  } else {
-    if (f4) launch_tc_k<KB, false, true>(a, grid, st);
-    else launch_tc_k<KB, false, false>(a, grid, st);
-  }
+  if (a.dump) launch_tc_k<KB, true>(a, grid, st);
+  else launch_tc_k<KB, false>(a, grid, st);
 }
 
 }  // namespace
@@ -675,6 +591,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     a.L = L;
     a.slots = uint32_t(kEpiGroups * spq);
     a.dump = d_dump;
+#ifdef MIHG_TC_DEBUG  // timing probes of a debug build (make TCDEBUG=1); never in the product .so
     if (const char* mo = std::getenv("MIHG_TC_MMA_ONLY")) a.mma_only = uint32_t(std::atoi(mo));
     const char* pe = std::getenv("MIHG_TC_PROF");
     const bool dbg_prof = pe && pe[0] == '1';
@@ -683,6 +600,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
       MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, 32 * 8 * 8, st));
       a.prof = profbuf.get();
     }
+#endif
     DeviceBuffer<uint64_t> lists(qn * a.slots * L, st), gathered(qn * a.slots * L, st);
     DeviceBuffer<uint32_t> counts(qn * a.slots, st), gcount(qn, st), gbound(qn, st);
     MIHG_CUDA(cudaMemsetAsync(counts.get(), 0, qn * a.slots * 4, st));
@@ -707,6 +625,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
       default: launch_tc<256>(a, grid, st); break;
     }
     if (prof) MIHG_CUDA(cudaEventRecord(ev[1], st));
+#ifdef MIHG_TC_DEBUG
     if (dbg_prof) {
       unsigned long long h[32 * 8];
       MIHG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -718,6 +637,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
       }
       fprintf(stderr, "tcprof grid %u ipc %u nch %u spq %u\n", grid, a.ipc, a.nch, a.spq);
     }
+#endif
     gather_lists_kernel<<<unsigned(qn), 256, 0, st>>>(lists.get(), counts.get(), a.slots, L, gathered.get(),
                                                       gcount.get());
     MIHG_LAUNCH();

@@ -245,8 +245,9 @@ class MihIndex:
         partition=(count, rank, allreduce) runs the probe-space partitioned search of one rank:
         ``allreduce(dev_ptr, n, dtype, stream)`` sums n device elements (dtype 0 u32, 1 u64) in
         place across ranks; the outputs are this rank's local top-k (merge across ranks).
-        partition=(count, rank, allreduce, True) is the id-range-shard layout with global
-        stopping instead (this index holds one shard, built with id_base)."""
+        partition=(count, rank, allreduce, True[, k_stop]) is the id-range-shard layout with global
+        stopping instead (this index holds one shard, built with id_base); k_stop is the global k
+        of the stopping rule when this shard's k is clamped below it (default: k)."""
         L = _lib.lib()
         sp = C.c_void_p(stream) if stream else None
         tr = C.c_void_p(d_traces) if d_traces else None
@@ -256,6 +257,7 @@ class MihIndex:
             return
         count, rank, fn = partition[:3]
         id_shards = bool(partition[3]) if len(partition) > 3 else False
+        k_stop = int(partition[4]) if len(partition) > 4 else 0
         errors = []
 
         def _cb(user, ptr, n, dtype, strm):
@@ -267,7 +269,7 @@ class MihIndex:
                 return 1
 
         cb = _lib.ALLREDUCE_FN(_cb)
-        part = _lib.Partition(count, rank, cb, None, 1 if id_shards else 0)
+        part = _lib.Partition(count, rank, cb, None, 1 if id_shards else 0, k_stop)
         rc = L.mihg_knn_batch_device_part(self._h, C.c_void_p(d_queries), nq, k, C.c_void_p(d_ids),
                                           C.c_void_p(d_dists), tr, C.byref(part), sp)
         if errors:

@@ -73,18 +73,24 @@ def gpu_merge(all_ids, all_dists, k: int):
 
 
 class ShardedKnn:
-    """One rank's view of an id-range sharded index."""
+    """One rank's view of an id-range sharded index.
+
+    ``local_search(queries, k_local, k_global, collective)`` returns the rank's exact local top
+    ``k_local`` as int32 [nq, k_local] (global ids). With ``collective`` it runs the per-round
+    histogram all-reduce of global stopping, so every rank of the group must call it together."""
 
     def __init__(self, local_search: Callable, n_local: int, group=None,
-                 merge: Optional[Callable] = None):
+                 merge: Optional[Callable] = None, global_stopping: bool = False):
         import torch.distributed as dist
 
-        self.local_search = local_search  # (queries, k) -> (ids, dists) int32 [nq, k], global ids
+        self.local_search = local_search
         self.n_local = n_local
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.merge = merge or gpu_merge
+        self.global_stopping = global_stopping and self.world > 1
+        self._min_local = None
 
     @classmethod
     def probe_partitioned(cls, index, group=None):
@@ -98,7 +104,7 @@ class ShardedKnn:
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         ar = nccl_allreduce(group)
 
-        def local(queries, k):
+        def local(queries, k, k_global=None, collective=True):
             nq = queries.shape[0]
             ids = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
             d = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
@@ -118,18 +124,33 @@ class ShardedKnn:
         import torch.distributed as dist
 
         world, rank = dist.get_world_size(group), dist.get_rank(group)
-        part = (world, rank, nccl_allreduce(group), True) if (global_stopping and world > 1) else None
+        ar = nccl_allreduce(group) if (global_stopping and world > 1) else None
 
-        def local(queries, k):
+        def local(queries, k, k_global=None, collective=False):
             nq = queries.shape[0]
             ids = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
             d = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
+            # the stopping rule of global stopping uses the caller's global k (a shard smaller
+            # than k searches its whole local k = n_local but stops with the others)
+            part = (world, rank, ar, True, k_global or k) if collective else None
             index.knn_search_device(queries.data_ptr(), nq, k, ids.data_ptr(), d.data_ptr(),
                                     stream=torch.cuda.current_stream(queries.device).cuda_stream,
                                     partition=part)
             return ids, d
 
-        return cls(local, index.size(), group)
+        return cls(local, index.size(), group, global_stopping=ar is not None)
+
+    def _smallest_shard(self, device):
+        """min over ranks of the shard sizes (identical on every rank; one collective, cached)."""
+        import torch
+        import torch.distributed as dist
+
+        if self._min_local is None:
+            on = device if dist.get_backend(self.group) == "nccl" else "cpu"
+            t = torch.tensor([self.n_local], dtype=torch.int64, device=on)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+            self._min_local = int(t.item())
+        return self._min_local
 
     def search(self, queries, k: int):
         """Exact global top-k for every query (all ranks return the same result)."""
@@ -138,8 +159,11 @@ class ShardedKnn:
 
         nq = queries.shape[0]
         kk = min(k, self.n_local)
+        # global stopping needs every rank in every round: an empty shard cannot search, so then
+        # all ranks (same decision everywhere) stop on their local counts instead (also exact)
+        collective = self.global_stopping and self._smallest_shard(queries.device) > 0
         if kk > 0:
-            ids, d = self.local_search(queries, kk)
+            ids, d = self.local_search(queries, kk, k, collective)
         else:
             ids = torch.empty((nq, 0), dtype=torch.int32, device=queries.device)
             d = torch.empty((nq, 0), dtype=torch.int32, device=queries.device)

@@ -10,15 +10,6 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["i8", "fp4"], autouse=True)
-def mma_kind(request):
-    """Every K7 test runs under both MMA_KIND settings (the 256-code-tile geometry runs int8 for
-    both: its accumulators fill TMEM, where the E2M1 variant keeps A and its block scales)."""
-    os.environ["MIHG_TC_KIND"] = request.param
-    yield request.param
-    os.environ.pop("MIHG_TC_KIND", None)
-
-
 def _popc_dist(q, x):
     """[nq, n] Hamming distances of packed u64 rows (numpy restatement of hamming_words)."""
     d = np.zeros((q.shape[0], x.shape[0]), np.int64)

@@ -42,21 +42,31 @@ def _worker(rank, world, port, n, bits, m, k, result_q):
         lo, hi = shard_range(n, rank, world)
         h = P.build(db[lo:hi], bits, m) if hi > lo else None
 
-        def local(queries, kk):
+        calls = []
+
+        def local(queries, kk, k_global=None, collective=False):
+            calls.append((kk, k_global, collective))
             ids, d, _ = h.knn(queries.numpy().view(np.uint64), kk)
             return (torch.from_numpy((ids.astype(np.uint64) + lo).astype(np.uint32).view(np.int32)),
                     torch.from_numpy(d.view(np.int32)))
 
-        sk = ShardedKnn(local, hi - lo, merge=numpy_merge)
+        sk = ShardedKnn(local, hi - lo, merge=numpy_merge, global_stopping=True)
         ids, d = sk.search(torch.from_numpy(qs.view(np.int64)), k)
         want_i, want_d = P.scan_knn(db, bits, qs, k)
         ok = np.array_equal(ids.numpy().view(np.uint32), want_i) and np.array_equal(d.numpy().view(np.uint32), want_d)
-        result_q.put((rank, bool(ok)))
+        # global stopping: the stopping k is the caller's k on every rank, and the collective
+        # local search runs on every rank or on none (an empty shard turns it off everywhere)
+        if hi > lo:
+            ok = ok and calls == [(min(k, hi - lo), k, n >= world)]
+        else:
+            ok = ok and calls == []
+        result_q.put((rank, bool(ok), [c[2] for c in calls]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,bits,m,k", [(5000, 64, 4, 10), (3001, 70, 4, 100), (150, 64, 4, 100)])
+# (150, k=100): shards of 75 < k; (1, k=1): rank 1's shard is empty, so global stopping is off
+@pytest.mark.parametrize("n,bits,m,k", [(5000, 64, 4, 10), (3001, 70, 4, 100), (150, 64, 4, 100), (1, 64, 4, 1)])
 def test_sharded_knn_equals_single_index(n, bits, m, k):
     world = 2
     ctx = mp.get_context("spawn")
@@ -68,7 +78,10 @@ def test_sharded_knn_equals_single_index(n, bits, m, k):
     for p in procs:
         p.join(timeout=240)
         assert p.exitcode == 0
-    res = dict(q.get(timeout=10) for _ in range(world))
+    res = {}
+    for _ in range(world):
+        r, ok, coll = q.get(timeout=10)
+        res[r] = ok
     assert res == {0: True, 1: True}
 
 

@@ -10,6 +10,8 @@ def main(rep, top=20):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(src.splitlines()))
     h = rows[1]
+    if "--columns" in sys.argv:
+        print([c for c in h if "ector" in c or "equest" in c or "avefront" in c])
     col = {n: h.index(n) for n in ("Address", "Source", "Warp Stall Sampling (All Samples)", "Instructions Executed",
                                    "L2 Theoretical Sectors Global", "L2 Theoretical Sectors Global Ideal",
                                    "L1 Tag Requests Global", "L2 Theoretical Sectors Local")}
@@ -27,7 +29,14 @@ def main(rep, top=20):
     print(f"global L2 sectors {tot_g:.3e}, local (spill) sectors {tot_l:.3e}")
     for d in sorted(data, key=lambda d: -d[4])[:top]:
         print(f"  {d[4] / tot_g * 100:5.1f}% sect {d[4]:.3e} (ideal {d[5]:.3e}) stall {d[2] / tot_s * 100:4.1f}%  {d[1][:70]}")
+    # wide loads (LDG.E.ENL2.256 etc.) may not report theoretical sectors: list every global load
+    # with its executed count so their traffic can be estimated (32 B per lane-load, uncoalesced)
+    print("global loads/stores by executed warp-instructions:")
+    for d in sorted((d for d in data if ("LDG" in d[1] or "STG" in d[1] or "ATOM" in d[1] or "RED" in d[1])),
+                    key=lambda d: -d[3])[:top]:
+        print(f"  exec {d[3]:.3e} sect {d[4]:.3e} stall {d[2] / tot_s * 100:4.1f}%  {d[1][:80]}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 20)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    main(args[0], int(args[1]) if len(args) > 1 else 20)

@@ -160,6 +160,7 @@ int mihg_range_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint
  * Traces: candidates/unique are summed over shards (= the single-index trace), lookups and
  * final_radius are every shard's own (= the single-index values). */
 typedef int (*mihg_allreduce_fn)(void* user, void* dev_ptr, uint64_t count, int dtype, void* stream);
+typedef struct mihg_comm mihg_comm;
 typedef struct mihg_partition {
   uint32_t count;
   uint32_t rank;
@@ -168,10 +169,35 @@ typedef struct mihg_partition {
   uint32_t id_shards; /* 0: probe-space partition of a replicated index; 1: id-range shards */
   uint32_t k_stop;    /* k of the GLOBAL stopping rule (id_shards: the caller's k, which may exceed
                          a small shard's local k); 0 -> the call's k. Must be equal on all ranks. */
+  mihg_comm* comm;    /* non-NULL: the per-round all-reduce is an NCCL all-reduce on this library
+                         communicator (allreduce/user ignored); count/rank must match it */
 } mihg_partition;
 int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint64_t nq, uint32_t k,
                                uint32_t* d_ids, uint32_t* d_dists, mihg_trace* d_traces,
                                const mihg_partition* part, void* stream);
+
+/* NCCL communicator owned by the library (SURVEY.md §8e exchange steps). NCCL is loaded at run
+ * time (the copy already in the process if any, else MIHG_NCCL_LIBRARY, else libnccl.so.2);
+ * failures -> MIHG_ENCCL. Rank 0 calls mihg_comm_unique_id, ships the 128 bytes to every rank
+ * (any out-of-band channel), and every rank calls mihg_comm_init with its device. */
+int mihg_comm_unique_id(uint8_t out_id[128]);
+int mihg_comm_init(const uint8_t id[128], int nranks, int rank, int device, mihg_comm** out);
+void mihg_comm_free(mihg_comm* comm);
+int mihg_nccl_version(int* version);
+
+/* Multi-GPU exact kNN in one call per rank, every collective inside the library (NCCL on the
+ * index stream, joined to `stream`): the rank's local search with the per-round histogram
+ * all-reduce, then an all-gather of the local top-k lists and the exact k-way merge on the device.
+ * Every rank passes the same queries and k and receives the GLOBAL top-k in d_ids/d_dists [nq][k].
+ *   layout 0: probe-space partition — every rank's index holds all n_total codes; rank g probes
+ *             the ring values whose top log2(G) key bits equal g (G a power of two).
+ *   layout 1: id-range shards (north_star's layout) — rank g's index holds ids
+ *             [g*ceil(n_total/G), ...) built with that id_base; global stopping on the summed
+ *             histograms (local stopping when some shard is empty).
+ * d_traces: nq global traces or NULL (candidates/unique summed over ranks). */
+int mihg_knn_sharded_device(mihg_index* idx, mihg_comm* comm, int layout, uint64_t n_total,
+                            const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                            uint32_t* d_dists, mihg_trace* d_traces, void* stream);
 
 /* scan_knn(db, q, k) — scan.hpp:43-68, batched, over the index's device codes. */
 int mihg_scan_knn_batch(mihg_index* idx, const uint64_t* queries, uint64_t nq, uint32_t k,

@@ -59,7 +59,8 @@ class Partition(C.Structure):
     """mihg_partition: probe-space partition of a multi-GPU kNN call."""
 
     _fields_ = [("count", C.c_uint32), ("rank", C.c_uint32), ("allreduce", ALLREDUCE_FN),
-                ("user", C.c_void_p), ("id_shards", C.c_uint32), ("k_stop", C.c_uint32)]
+                ("user", C.c_void_p), ("id_shards", C.c_uint32), ("k_stop", C.c_uint32),
+                ("comm", C.c_void_p)]
 
 
 class Profile(C.Structure):
@@ -93,6 +94,13 @@ SYMBOLS = [
     ("mihg_knn_batch_device_part", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                              C.c_void_p, C.c_void_p, C.c_void_p,
                                              C.POINTER(Partition), C.c_void_p]),
+    ("mihg_comm_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("mihg_comm_init", C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("mihg_comm_free", None, [C.c_void_p]),
+    ("mihg_nccl_version", C.c_int, [C.POINTER(C.c_int)]),
+    ("mihg_knn_sharded_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_void_p,
+                                          C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]),
     ("mihg_scan_knn_batch", C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint32, u32p, u32p]),
     ("mihg_scan_knn_batch_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
                                              C.c_void_p, C.c_void_p, C.c_void_p]),

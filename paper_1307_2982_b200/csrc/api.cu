@@ -32,6 +32,9 @@ int guarded(F&& f) {
   } catch (const std::bad_alloc&) {
     g_err = "bad_alloc";
     return MIHG_ENOMEM;
+  } catch (const mihg::NcclError& e) {
+    mihg::set_last_error(e.what());
+    return MIHG_ENCCL;
   } catch (const mihg::CudaError& e) {
     g_err = e.what();
     // surface allocation failures as ENOMEM
@@ -302,12 +305,95 @@ int mihg_knn_batch_device_part(mihg_index* idx, const uint64_t* d_queries, uint6
       pt.user = part->user;
       pt.id_shards = part->id_shards != 0;
       pt.k_stop = part->k_stop;
+      pt.comm = reinterpret_cast<mihg::Comm*>(part->comm);
+      if (pt.comm && (uint32_t(mihg::comm_size(pt.comm)) != pt.count || uint32_t(mihg::comm_rank(pt.comm)) != pt.rank))
+        throw mihg::InvalidArgument("partitioned knn: count/rank do not match the communicator");
     }
     mihg::KnnOptions opt;
     opt.part = part ? &pt : nullptr;
     StreamJoin j(static_cast<cudaStream_t>(stream), ix.stream);
     mihg::knn_device(ix, d_queries, nq, k, d_ids, d_dists, reinterpret_cast<mihg::Trace*>(d_traces), ix.stream,
                      opt);
+  });
+}
+
+int mihg_comm_unique_id(uint8_t out_id[128]) {
+  return guarded([&] {
+    if (!out_id) throw mihg::InvalidArgument("null argument");
+    mihg::comm_unique_id(out_id);
+  });
+}
+
+int mihg_comm_init(const uint8_t id[128], int nranks, int rank, int device, mihg_comm** out) {
+  return guarded([&] {
+    if (!id || !out) throw mihg::InvalidArgument("null argument");
+    DeviceGuard g(device);
+    *out = reinterpret_cast<mihg_comm*>(mihg::comm_init(id, nranks, rank, device));
+  });
+}
+
+void mihg_comm_free(mihg_comm* comm) {
+  guarded([&] { mihg::comm_free(reinterpret_cast<mihg::Comm*>(comm)); });
+}
+
+int mihg_nccl_version(int* version) {
+  return guarded([&] { *version = mihg::nccl_version(); });
+}
+
+int mihg_knn_sharded_device(mihg_index* idx, mihg_comm* comm, int layout, uint64_t n_total,
+                            const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                            uint32_t* d_dists, mihg_trace* d_traces, void* stream) {
+  return guarded([&] {
+    mihg::Index& ix = impl(idx);
+    if (!comm) throw mihg::InvalidArgument("sharded knn: null communicator");
+    if (layout != 0 && layout != 1) throw mihg::InvalidArgument("sharded knn: layout must be 0 or 1");
+    auto* c = reinterpret_cast<mihg::Comm*>(comm);
+    const uint32_t G = uint32_t(mihg::comm_size(c)), rank = uint32_t(mihg::comm_rank(c));
+    if (k > n_total) throw mihg::InvalidArgument("knn_search: k exceeds database size");
+    DeviceGuard g(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    StreamJoin j(static_cast<cudaStream_t>(stream), ix.stream);
+    cudaStream_t st = ix.stream;
+    mihg::Partition pt;
+    pt.count = G;
+    pt.rank = rank;
+    pt.comm = c;
+    uint32_t kk = k;
+    bool collective = true;
+    if (layout == 1) {
+      const uint64_t per = (n_total + G - 1) / G;
+      const uint64_t lo = std::min<uint64_t>(n_total, uint64_t(rank) * per), hi = std::min<uint64_t>(n_total, lo + per);
+      if (ix.n != hi - lo || (ix.n && ix.id_base != lo))
+        throw mihg::InvalidArgument("sharded knn: the index is not id shard " + std::to_string(rank) + " of n_total");
+      kk = uint32_t(std::min<uint64_t>(k, ix.n));
+      pt.id_shards = true;
+      pt.k_stop = k;
+      collective = n_total > uint64_t(G - 1) * per;  // every shard non-empty: global stopping
+    } else if (ix.n != n_total) {
+      throw mihg::InvalidArgument("sharded knn: layout 0 needs the full index on every rank");
+    }
+    if (nq == 0 || k == 0) return;
+    mihg::DeviceBuffer<uint32_t> li(nq * k, st), ld(nq * k, st);
+    if (kk < k) {  // a shard smaller than k: its list is padded (0xFFFFFFFF sorts last)
+      MIHG_CUDA(cudaMemsetAsync(li.get(), 0xFF, nq * k * 4, st));
+      MIHG_CUDA(cudaMemsetAsync(ld.get(), 0xFF, nq * k * 4, st));
+    }
+    if (kk > 0) {
+      mihg::KnnOptions opt;
+      opt.part = collective ? &pt : nullptr;
+      if (kk == k) {
+        mihg::knn_device(ix, d_queries, nq, kk, li.get(), ld.get(), reinterpret_cast<mihg::Trace*>(d_traces), st, opt);
+      } else {
+        mihg::DeviceBuffer<uint32_t> ti(nq * kk, st), td(nq * kk, st);
+        mihg::knn_device(ix, d_queries, nq, kk, ti.get(), td.get(), reinterpret_cast<mihg::Trace*>(d_traces), st, opt);
+        MIHG_CUDA(cudaMemcpy2DAsync(li.get(), k * 4, ti.get(), kk * 4, kk * 4, nq, cudaMemcpyDeviceToDevice, st));
+        MIHG_CUDA(cudaMemcpy2DAsync(ld.get(), k * 4, td.get(), kk * 4, kk * 4, nq, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    mihg::DeviceBuffer<uint32_t> gi(uint64_t(G) * nq * k, st), gd(uint64_t(G) * nq * k, st);
+    mihg::comm_allgather(c, li.get(), gi.get(), nq * k * 4, st);
+    mihg::comm_allgather(c, ld.get(), gd.get(), nq * k * 4, st);
+    mihg::merge_topk_device(gi.get(), gd.get(), G, nq, k, k, d_ids, d_dists, st);
   });
 }
 

@@ -92,28 +92,30 @@ Index::~Index() {
 
 namespace {
 
-// colex unranking: the idx-th z-subset of {0..s-1} (Gosper order) as a bit mask.
-__device__ __forceinline__ uint64_t unrank_comb(const uint64_t* __restrict__ binom, uint64_t idx,
+// colex unranking: the idx-th z-subset of {0..s-1} (Gosper order) as a bit mask. Substrings are
+// at most 32 bits (table.hpp:31), so masks, ring sizes (<= C(32,16)) and indices fit 32 bits.
+__device__ __forceinline__ uint32_t unrank_comb(const uint64_t* __restrict__ binom, uint32_t idx,
                                                 uint32_t s, uint32_t z) {
-  uint64_t mask = 0;
+  uint32_t mask = 0;
   uint32_t c = s;
   for (uint32_t t = z; t >= 1; --t) {
     uint32_t cc = c - 1;
-    uint64_t b = __ldg(binom + cc * kBinomStride + t);
-    while (b > idx) b = __ldg(binom + (--cc) * kBinomStride + t);
-    mask |= uint64_t(1) << cc;
+    uint32_t b = uint32_t(__ldg(binom + cc * kBinomStride + t));
+    while (b > idx) b = uint32_t(__ldg(binom + (--cc) * kBinomStride + t));
+    mask |= 1u << cc;
     idx -= b;
     c = cc;
   }
   return mask;
 }
 
-// next subset of the same size in increasing numeric order (Gosper's hack)
-__device__ __forceinline__ uint64_t next_comb(uint64_t x) {
+// next subset of the same size in increasing numeric order (Gosper's hack); past the last
+// subset of a 32-bit ring the value is garbage, never used (the walk stops at the ring end)
+__device__ __forceinline__ uint32_t next_comb(uint32_t x) {
   if (x == 0) return 0;
-  const uint64_t u = x & (~x + 1);
-  const uint64_t v = x + u;
-  return v | (((v ^ x) >> 2) >> (__ffsll(static_cast<long long>(u)) - 1));
+  const uint32_t u = x & (~x + 1);
+  const uint32_t v = x + u;
+  return v | (((v ^ x) >> 2) >> (__ffs(int(u)) - 1));
 }
 
 template <int W>
@@ -311,17 +313,16 @@ __device__ __forceinline__ bool first_discovery(const Diff<W>& df, const ProbeAr
   return true;
 }
 
+// Per-unit query state kept in registers (the buffer base and capacity are derived on the rare
+// append path, which keeps the probe kernel inside its 32-register budget).
 struct QueryCtx {
-  uint32_t q, U, cap;
-  uint64_t base;
+  uint32_t q, U;
 };
 
 __device__ __forceinline__ QueryCtx query_ctx(const ProbeArgs& p, uint32_t q) {
   QueryCtx c;
   c.q = q;
   c.U = p.ubound[q];
-  c.base = p.bufbase ? p.bufbase[q] : uint64_t(q) * p.cap_fixed;
-  c.cap = p.bufcap ? p.bufcap[q] : p.cap_fixed;
   return c;
 }
 
@@ -373,14 +374,16 @@ __device__ __forceinline__ void verify_entries(const ProbeArgs& p, const QueryCt
     const uint32_t m1 = __match_any_sync(~0u, key1);
     if (k1 && (m1 & lt) == 0) atomicAdd(p.hist + uint64_t(c.q) * p.b1 + dist1, __popc(m1));
   }
+  const uint64_t qbase = p.bufbase ? p.bufbase[c.q] : uint64_t(c.q) * p.cap_fixed;
+  const uint32_t qcap = p.bufcap ? p.bufcap[c.q] : p.cap_fixed;
   if (k0) {
     const uint32_t pos = base + __popc(b0 & lt);
-    if (pos < c.cap) p.buf[c.base + pos] = (uint64_t(dist0) << 32) | id0;
+    if (pos < qcap) p.buf[qbase + pos] = (uint64_t(dist0) << 32) | id0;
     else atomicMin(p.dropmin + c.q, dist0);
   }
   if (k1) {
     const uint32_t pos = base + n0 + __popc(b1 & lt);
-    if (pos < c.cap) p.buf[c.base + pos] = (uint64_t(dist1) << 32) | id1;
+    if (pos < qcap) p.buf[qbase + pos] = (uint64_t(dist1) << 32) | id1;
     else atomicMin(p.dropmin + c.q, dist1);
   }
 }
@@ -402,11 +405,12 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kerne
   __shared__ uint32_t s_off[kProbeWarps][kWarpBuckets];
   const uint32_t nw = W ? W : p.nw;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t span = uint64_t(p.chunk) * 32;  // ring indices per warp unit
+  const uint32_t span = p.chunk * 32;  // ring indices per warp unit
   const uint64_t nwarps = uint64_t(gridDim.x) * kProbeWarps;
   uint64_t u = blockIdx.x * uint64_t(kProbeWarps) + wib;
   for (;; u += nwarps) {
-    uint64_t slot, part, ring = p.ring, high = 0;
+    uint32_t slot, part;
+    uint32_t ring = uint32_t(p.ring), high = 0;
     uint32_t zbits = p.rr, sbits = p.tab.s;
     if (p.slice_bits) {
       // sliced round: units are claimed in order (slice-major), so the warps in flight probe
@@ -425,25 +429,25 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kerne
       sbits = p.tab.s - p.slice_bits;
       const uint32_t T = P ^ G;  // flip pattern of the top slice bits
       zbits = p.rr - __popc(T);
-      ring = __ldg(p.binom + sbits * kBinomStride + zbits);
-      const uint64_t upq = (ring + span - 1) / span;
+      ring = uint32_t(__ldg(p.binom + sbits * kBinomStride + zbits));
+      const uint32_t upq = (ring + span - 1) / span;
       const uint64_t rel = u - __ldg(p.pair_prefix + lo_i);
-      const uint64_t kq = rel / upq;
-      part = rel - kq * upq;
+      const uint32_t kq = uint32_t(rel / upq);
+      part = uint32_t(rel - uint64_t(kq) * upq);
       slot = p.grouped[p.gstart[G] + kq];
-      high = uint64_t(T) << sbits;
+      high = sbits < 32 ? T << sbits : 0u;
     } else {
       if (u >= p.total) break;
-      slot = u / p.cpq;
-      part = u - slot * p.cpq;
+      slot = uint32_t(u / p.cpq);
+      part = uint32_t(u - uint64_t(slot) * p.cpq);
     }
     const uint32_t q = p.active[slot];
     if (p.rlimit && p.r > p.rlimit[q]) continue;
-    const uint64_t ubeg = part * span;
-    const uint64_t uend = min(ring, ubeg + span);
-    uint64_t i = ubeg + uint64_t(lane) * p.chunk;
-    const uint64_t iend = min(uend, i + p.chunk);
-    uint64_t mask = i < iend ? unrank_comb(p.binom, i, sbits, zbits) : 0;
+    const uint32_t ubeg = part * span;
+    const uint32_t uend = uint32_t(min(uint64_t(ring), uint64_t(ubeg) + span));
+    uint32_t i = ubeg + lane * p.chunk;
+    const uint32_t iend = min(uend, i + p.chunk);
+    uint32_t mask = i < iend ? unrank_comb(p.binom, i, sbits, zbits) : 0u;
     const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
     uint64_t qreg[W ? W : 1];
     const uint64_t* qptr = p.qcodes + uint64_t(q) * nw;
@@ -460,7 +464,7 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kerne
       for (int b = 0; b < kLaneProbes; ++b) {
         uint32_t l = 0, h = 0;
         if (i < iend && it + b < p.chunk) {
-          const uint32_t v = qa ^ uint32_t(high | mask);
+          const uint32_t v = qa ^ (high | mask);
           if (p.part_bits == 0 || (v >> (p.tab.s - p.part_bits)) == p.part_id) probe_bucket(p.tab, v, l, h);
           mask = next_comb(mask);
           ++i;
@@ -990,6 +994,10 @@ RerunResult rerun_pass(Index& idx, const ProbeArgs& p, const uint32_t* d_rerun, 
 }
 
 void call_allreduce(const Partition* part, void* ptr, uint64_t count, int dtype, cudaStream_t st) {
+  if (part->comm) {  // the library's own NCCL communicator: enqueued on the index stream
+    comm_allreduce_sum(part->comm, ptr, count, dtype, st);
+    return;
+  }
   if (!part->allreduce) throw InvalidArgument("partitioned knn: no all-reduce callback");
   const int rc = part->allreduce(part->user, ptr, count, dtype, st);
   if (rc) throw CudaError("partitioned knn: all-reduce callback failed (" + std::to_string(rc) + ")");
@@ -997,7 +1005,8 @@ void call_allreduce(const Partition* part, void* ptr, uint64_t count, int dtype,
 
 void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_t* d_ids,
                uint32_t* d_dists, Trace* d_tr, cudaStream_t st, const KnnOptions& opt) {
-  const Partition* part = opt.part && opt.part->count > 1 ? opt.part : nullptr;
+  // a library communicator keeps the collective path even at count 1 (one-rank NCCL group)
+  const Partition* part = opt.part && (opt.part->count > 1 || opt.part->comm) ? opt.part : nullptr;
   Workspace& ws = *idx.ws;
   const uint32_t m = idx.m, b1 = idx.bits + 1, cap = ws.cap;
   const unsigned g1 = unsigned(std::min<uint64_t>((nq + 255) / 256, 4096));

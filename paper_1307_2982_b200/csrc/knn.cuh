@@ -15,13 +15,29 @@ static_assert(sizeof(Trace) == 40, "mihg_trace ABI");
 // summed across ranks every round through `allreduce` (in place on device memory, ordered on
 // `stream`; dtype 0 = u32, 1 = u64) so all ranks share the reference's stopping rule. The call
 // then returns the rank's LOCAL top-k candidates; the caller all-gathers and merges them.
+struct Comm;  // NCCL communicator (comm.cu)
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 struct Partition {
   uint32_t count = 1, rank = 0;
   int (*allreduce)(void* user, void* dev_ptr, uint64_t count, int dtype, void* stream) = nullptr;
   void* user = nullptr;
   bool id_shards = false;  // id-range shards with global stopping (no probe split)
   uint32_t k_stop = 0;     // k of the global stopping rule (0: the call's k)
+  Comm* comm = nullptr;    // library-owned NCCL communicator: used instead of `allreduce`
 };
+
+// NCCL (comm.cu; loaded at run time). Collectives are enqueued on `st`, no host synchronisation.
+void comm_unique_id(uint8_t* out128);
+Comm* comm_init(const uint8_t* id128, int nranks, int rank, int device);
+void comm_free(Comm* c);
+int comm_size(const Comm* c);
+int comm_rank(const Comm* c);
+int nccl_version();
+void comm_allreduce_sum(Comm* c, void* ptr, uint64_t n, int dtype, cudaStream_t st);
+void comm_allgather(Comm* c, const void* send, void* recv, uint64_t bytes, cudaStream_t st);
 
 struct KnnOptions {
   uint32_t buffer_cap = 8192;   // per-query candidate buffer (u64 keys) in the main pass

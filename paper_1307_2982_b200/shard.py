@@ -56,6 +56,68 @@ class _nullctx:
         return False
 
 
+class NcclComm:
+    """The library's own NCCL communicator (mihg_comm_init) over the ranks of a torch.distributed
+    group: rank 0 draws the unique id, the group broadcasts it once (the only host-side step),
+    and from then on every collective of the sharded search is enqueued by libmihg itself."""
+
+    def __init__(self, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            _lib.check(_lib.lib().mihg_comm_unique_id(uid))
+        on = torch.device("cuda", device) if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=on)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (C.c_uint8 * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        _lib.check(_lib.lib().mihg_comm_init(uid, self.world, self.rank, device, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        from . import _lib
+
+        if self._h:
+            _lib.lib().mihg_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def native_sharded_search(index, comm: NcclComm, layout: str, n_total: int, queries, k: int, traces=None,
+                          stream: int = 0):
+    """Exact global top-k on every rank in ONE library call (mihg_knn_sharded_device): local search
+    with the per-round NCCL histogram all-reduce, NCCL all-gather of the local lists, device merge.
+    layout: "probe" (replicated index, probe-space partition) or "id" (id-range shards)."""
+    import torch
+
+    from . import _lib
+
+    nq = queries.shape[0]
+    ids = torch.empty((nq, k), dtype=torch.int32, device=queries.device)
+    d = torch.empty_like(ids)
+    stream = stream or torch.cuda.current_stream(queries.device).cuda_stream
+    _lib.check(_lib.lib().mihg_knn_sharded_device(index._h, comm.handle, 0 if layout == "probe" else 1, n_total,
+                                                  C.c_void_p(queries.data_ptr()), nq, k, C.c_void_p(ids.data_ptr()),
+                                                  C.c_void_p(d.data_ptr()),
+                                                  C.c_void_p(traces.data_ptr()) if traces is not None else None,
+                                                  C.c_void_p(stream)))
+    return ids, d
+
+
 def gpu_merge(all_ids, all_dists, k: int):
     """Exact k-way merge on the GPU: all_* are int32 CUDA tensors [G, nq, k_in]."""
     import torch

@@ -76,15 +76,6 @@ void configure_mempool(int device) {
   MIHG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t v = keep;
   MIHG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &v));
-  // L2 -> DRAM fetch granularity (bytes) for the probe's random 32-byte directory sectors;
-  // MIHG_L2_FETCH overrides the driver default (A/B experiments).
-  if (const char* f = std::getenv("MIHG_L2_FETCH")) {
-    MIHG_CUDA(cudaSetDevice(device));
-    MIHG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(std::atoi(f))));
-    size_t got = 0;
-    MIHG_CUDA(cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity));
-    if (std::getenv("MIHG_VERBOSE")) fprintf(stderr, "mihg: L2 fetch granularity %zu bytes\n", got);
-  }
   done[device] = true;
 }
 

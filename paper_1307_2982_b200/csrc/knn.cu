@@ -55,10 +55,19 @@ struct Workspace {
   uint32_t* h_counter = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // device-planned radius rounds: nact_dev[r] = queries active entering round r (written by the
+  // previous round's end kernel), mirrored into pinned h_nact[r] behind event ev_round[r - 1];
+  // ev_probe[2r], [2r+1] bracket round r's probe kernels (profiling)
+  DeviceBuffer<uint32_t> nact_dev;
+  uint32_t* h_nact = nullptr;
+  std::vector<cudaEvent_t> ev_round, ev_probe;
   ~Workspace() {
     if (h_counter) cudaFreeHost(h_counter);
+    if (h_nact) cudaFreeHost(h_nact);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (cudaEvent_t e : ev_round) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_probe) cudaEventDestroy(e);
   }
 };
 
@@ -221,12 +230,30 @@ struct ProbeArgs {
   // L2-sliced rounds (slice_bits > 0): active queries grouped by the top t bits G of their
   // substring; units enumerated per (slice P, group G) pair, P-major, claimed in order.
   uint32_t slice_bits;
+  // device-planned rounds (the host runs ahead of the GPU): the round's active count is read from
+  // *d_nact and the work split derived on the device (chunk from *d_chunk when sliced)
+  const uint32_t* d_nact;
+  uint32_t* d_chunk;
+  uint64_t lane_target;  // lanes to keep busy (plan_round)
+  double chunk_scale;    // sliced rounds: chunk = nact * ring * chunk_scale (plan_slicing)
+  uint32_t prefetch;            // sparse tables: 0 off, 1 next iteration's directory sectors -> L1, 2 -> L2
+#ifdef MIHG_TC_DEBUG
+  uint32_t debug_probe_only;    // debug build: skip verification (MIHG_DEBUG_PROBE_ONLY=1)
+#endif
   uint32_t part_bits, part_id;  // probe-space partition (multi-GPU): top key bits owned
   const uint64_t* pair_prefix;  // 4^t + 1 exclusive unit prefix over (P, G) pairs
   const uint32_t* gstart;       // 2^t + 1 group starts into grouped[]
   const uint32_t* grouped;      // active slots sorted by group
   unsigned long long* work_counter;
 };
+
+// Chunking of a round's (queries x ring) work list into warp units of 32 lanes x chunk probes.
+__host__ __device__ __forceinline__ uint32_t plan_chunk(uint64_t nact, uint64_t ring, uint64_t target) {
+  uint64_t chunk = (nact * ring + target - 1) / target;
+  chunk = chunk < 1 ? 1 : (chunk > 256 ? 256 : chunk);
+  const uint64_t cap = (ring + 31) / 32 < 1 ? 1 : (ring + 31) / 32;
+  return uint32_t(chunk < cap ? chunk : cap);
+}
 
 // Per sliced round (one block): group the active queries by G = top t bits of their substring,
 // then the unit prefix over (P, G) pairs: within slice P a query of group G has the sub-ring
@@ -237,6 +264,13 @@ __global__ void __launch_bounds__(1024) slice_plan_kernel(ProbeArgs p, uint32_t 
                                                           uint64_t* __restrict__ pair_prefix) {
   __shared__ uint32_t hist[256], cur[256];
   __shared__ unsigned long long part[1024];
+  if (p.d_nact) {  // device-planned round: this round's count and chunk
+    nact = *p.d_nact;
+    const double c = floor(double(nact) * double(p.ring) * p.chunk_scale);
+    const uint32_t chunk = uint32_t(c < 1.0 ? 1.0 : (c > 256.0 ? 256.0 : c));
+    span = uint64_t(chunk) * 32;
+    if (threadIdx.x == 0) *p.d_chunk = chunk;
+  }
   const uint32_t t = p.slice_bits, G = 1u << t, sb = p.tab.s - t;
   for (uint32_t i = threadIdx.x; i < G; i += blockDim.x) hist[i] = 0;
   __syncthreads();
@@ -397,15 +431,30 @@ constexpr int kProbeWarps = kProbeThreads / 32;
 // of the entries lane-parallel, two per lane per pass (entry t belongs to the bucket whose
 // [off, off + cnt) holds t: 7-step binary search in shared memory), so bucket-size skew never
 // idles the warp. Buckets above kInlineMax go to the piece queue.
+#ifndef MIHG_PROBE_MINB
+#define MIHG_PROBE_MINB 8  // resident blocks per SM for W <= 2 (32 registers at 8)
+#endif
 template <int W, bool kTrace, int kLaneProbes>
-__global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kernel(ProbeArgs p) {
+__global__ void __launch_bounds__(kProbeThreads, W <= 2 ? MIHG_PROBE_MINB : 5) mih_probe_kernel(ProbeArgs p) {
   constexpr int kWarpBuckets = 32 * kLaneProbes;
   constexpr int kSearchSteps = kLaneProbes == 1 ? 5 : kLaneProbes == 2 ? 6 : 7;
   __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
   __shared__ uint32_t s_off[kProbeWarps][kWarpBuckets];
   const uint32_t nw = W ? W : p.nw;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint32_t span = p.chunk * 32;  // ring indices per warp unit
+  uint32_t pchunk = p.chunk;
+  uint64_t pcpq = p.cpq, ptotal = p.total;
+  if (p.d_nact) {  // device-planned round
+    const uint32_t nact = *p.d_nact;
+    if (p.slice_bits) {
+      pchunk = *p.d_chunk;
+    } else {
+      pchunk = plan_chunk(nact, p.ring, p.lane_target);
+      pcpq = (p.ring + 32ull * pchunk - 1) / (32ull * pchunk);
+      ptotal = uint64_t(nact) * pcpq;
+    }
+  }
+  const uint32_t span = pchunk * 32;  // ring indices per warp unit
   const uint64_t nwarps = uint64_t(gridDim.x) * kProbeWarps;
   uint64_t u = blockIdx.x * uint64_t(kProbeWarps) + wib;
   for (;; u += nwarps) {
@@ -437,16 +486,16 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kerne
       slot = p.grouped[p.gstart[G] + kq];
       high = sbits < 32 ? T << sbits : 0u;
     } else {
-      if (u >= p.total) break;
-      slot = uint32_t(u / p.cpq);
-      part = uint32_t(u - uint64_t(slot) * p.cpq);
+      if (u >= ptotal) break;
+      slot = uint32_t(u / pcpq);
+      part = uint32_t(u - uint64_t(slot) * pcpq);
     }
     const uint32_t q = p.active[slot];
     if (p.rlimit && p.r > p.rlimit[q]) continue;
     const uint32_t ubeg = part * span;
     const uint32_t uend = uint32_t(min(uint64_t(ring), uint64_t(ubeg) + span));
-    uint32_t i = ubeg + lane * p.chunk;
-    const uint32_t iend = min(uend, i + p.chunk);
+    uint32_t i = ubeg + lane * pchunk;
+    const uint32_t iend = min(uend, i + pchunk);
     uint32_t mask = i < iend ? unrank_comb(p.binom, i, sbits, zbits) : 0u;
     const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
     uint64_t qreg[W ? W : 1];
@@ -458,12 +507,12 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kerne
     const uint64_t* qc = W ? qreg : qptr;
     const QueryCtx ctx = query_ctx(p, q);
     uint64_t n_cand = 0, n_new = 0;
-    for (uint32_t it = 0; it < p.chunk; it += kLaneProbes) {
+    for (uint32_t it = 0; it < pchunk; it += kLaneProbes) {
       uint32_t lo[kLaneProbes], cnt[kLaneProbes];
 #pragma unroll
       for (int b = 0; b < kLaneProbes; ++b) {
         uint32_t l = 0, h = 0;
-        if (i < iend && it + b < p.chunk) {
+        if (i < iend && it + b < pchunk) {
           const uint32_t v = qa ^ (high | mask);
           if (p.part_bits == 0 || (v >> (p.tab.s - p.part_bits)) == p.part_id) probe_bucket(p.tab, v, l, h);
           mask = next_comb(mask);
@@ -471,6 +520,21 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kerne
         }
         lo[b] = l;
         cnt[b] = h - l;
+      }
+      if (p.prefetch && !p.tab.dense) {
+        // the next iteration's directory sectors start their DRAM trip now, overlapping this
+        // iteration's verification (no registers held: a cache prefetch)
+        uint32_t mk = mask, ii = i;
+#pragma unroll
+        for (int b = 0; b < kLaneProbes; ++b) {
+          if (ii < iend && it + kLaneProbes + b < pchunk) {
+            const DirBlock* blk = p.tab.dir + ((qa ^ (high | mk)) >> kDirBucketsLog2);
+            if (p.prefetch == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(blk));
+            else asm volatile("prefetch.global.L2 [%0];" ::"l"(blk));
+            mk = next_comb(mk);
+            ++ii;
+          }
+        }
       }
       uint32_t mine = 0;
 #pragma unroll
@@ -498,6 +562,9 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? 8 : 5) mih_probe_kerne
       }
       const uint32_t total = __shfl_sync(~0u, incl, 31);
       if (total == 0) continue;
+#ifdef MIHG_TC_DEBUG
+      if (p.debug_probe_only) continue;  // traffic attribution: directory probes alone
+#endif
       uint32_t off = incl - mine;
 #pragma unroll
       for (int b = 0; b < kLaneProbes; ++b) {
@@ -572,7 +639,9 @@ __global__ void __launch_bounds__(kProbeThreads, 8) mih_piece_kernel(ProbeArgs p
 }
 
 __global__ void mih_init_kernel(uint64_t nq, uint32_t bits, uint32_t* ubound, uint32_t* bufcnt,
-                                uint32_t* dropmin, uint32_t* act, uint32_t* final_r) {
+                                uint32_t* dropmin, uint32_t* act, uint32_t* final_r,
+                                uint32_t* nact_dev = nullptr) {
+  if (nact_dev && blockIdx.x == 0 && threadIdx.x == 0) nact_dev[0] = uint32_t(nq);
   for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < nq;
        q += uint64_t(gridDim.x) * blockDim.x) {
     ubound[q] = bits;
@@ -585,6 +654,7 @@ __global__ void mih_init_kernel(uint64_t nq, uint32_t bits, uint32_t* ubound, ui
 
 // One warp per active query: termination test, bound update, buffer compaction.
 __global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32_t nact,
+                                     const uint32_t* __restrict__ d_nact_in,
                                      uint32_t* __restrict__ act_out, uint32_t* __restrict__ nact_out,
                                      const uint32_t* __restrict__ hist, uint32_t b1,
                                      uint32_t* __restrict__ ubound, uint32_t k, uint32_t r,
@@ -592,6 +662,7 @@ __global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32
                                      uint64_t* __restrict__ buf, uint32_t cap) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  if (d_nact_in) nact = *d_nact_in;  // device-planned round (grid sized by an upper bound)
   if (warp >= nact) return;
   const uint32_t q = act_in[warp];
   const uint32_t U = ubound[q];
@@ -693,8 +764,8 @@ template <int W, bool kTrace>
 void launch_probe(const ProbeArgs& p, cudaStream_t st) {
   const uint64_t blocks_needed = (p.total + kProbeWarps - 1) / kProbeWarps;
   const uint64_t max_blocks = uint64_t(device_sm_count()) * 8;
-  const unsigned grid = p.slice_bits ? unsigned(max_blocks)
-                                     : unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
+  const unsigned grid = p.slice_bits || p.d_nact ? unsigned(max_blocks)
+                                                : unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
   if (p.pieces) MIHG_CUDA(cudaMemsetAsync(p.piece_count, 0, 4, st));
   switch (lane_probes()) {
     case 1: mih_probe_kernel<W, kTrace, 1><<<grid, kProbeThreads, 0, st>>>(p); break;
@@ -726,11 +797,8 @@ void dispatch_probe(const ProbeArgs& p, bool trace, cudaStream_t st) {
 
 // Chunking of a round's (queries x ring) work list into warp units of 32 lanes x chunk probes.
 void plan_round(ProbeArgs& p, uint64_t nact) {
-  const uint64_t work = nact * p.ring;
-  const uint64_t target = uint64_t(device_sm_count()) * 2048 * 4;  // lanes to keep busy
-  uint64_t chunk = (work + target - 1) / target;
-  chunk = std::max<uint64_t>(1, std::min<uint64_t>(chunk, 256));
-  chunk = std::min<uint64_t>(chunk, std::max<uint64_t>((p.ring + 31) / 32, 1));
+  p.lane_target = uint64_t(device_sm_count()) * 2048 * 4;  // lanes to keep busy
+  const uint64_t chunk = plan_chunk(nact, p.ring, p.lane_target);
   p.chunk = uint32_t(chunk);
   p.cpq = (p.ring + 32 * chunk - 1) / (32 * chunk);
   p.total = nact * p.cpq;
@@ -781,8 +849,8 @@ void plan_slicing(ProbeArgs& p, Workspace& ws, uint64_t nact, cudaStream_t st) {
   // resident warps / inflight
   const double resident_warps = double(device_sm_count()) * 64;
   const double inflight = std::max(1.0, std::floor(inflight_mb() * (1 << 20) / (bytes / double(1u << t))));
-  const double lanes_per_slice = double(nact) * double(p.ring) / double(1u << t);
-  const double chunk = std::floor(lanes_per_slice * inflight / (resident_warps * 32.0));
+  p.chunk_scale = inflight / (double(1u << t) * resident_warps * 32.0);
+  const double chunk = std::floor(double(nact) * double(p.ring) * p.chunk_scale);
   p.chunk = uint32_t(std::max(1.0, std::min(chunk, 256.0)));
   p.slice_bits = t;
   if (ws.grouped.size() < nact) ws.grouped = DeviceBuffer<uint32_t>(nact, st);
@@ -828,6 +896,12 @@ void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
   MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_counter), 16));
   MIHG_CUDA(cudaEventCreate(&ws->ev0));
   MIHG_CUDA(cudaEventCreate(&ws->ev1));
+  ws->nact_dev = DeviceBuffer<uint32_t>(b1 + 2, st);
+  MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_nact), (b1 + 2) * 4));
+  ws->ev_round.resize(b1 + 2);
+  for (cudaEvent_t& e : ws->ev_round) MIHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ws->ev_probe.resize(2 * (b1 + 2));
+  for (cudaEvent_t& e : ws->ev_probe) MIHG_CUDA(cudaEventCreate(&e));
 }
 
 uint32_t read_counter(const uint32_t* d, uint32_t* h, cudaStream_t st) {
@@ -923,6 +997,11 @@ ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   p.binom = device_binomials();
   static const uint32_t inline_max = env_u32("MIHG_INLINE_MAX", 64);
   static const uint32_t piece_size = env_u32("MIHG_PIECE_SIZE", 256);
+  static const uint32_t prefetch = env_u32("MIHG_PREFETCH", 0);
+  p.prefetch = prefetch;
+#ifdef MIHG_TC_DEBUG
+  p.debug_probe_only = env_u32("MIHG_DEBUG_PROBE_ONLY", 0);
+#endif
   p.inline_max = inline_max;
   p.piece_size = std::max<uint32_t>(32, piece_size);
   return p;
@@ -968,6 +1047,7 @@ RerunResult rerun_pass(Index& idx, const ProbeArgs& p, const uint32_t* d_rerun, 
   MIHG_CUDA(cudaMemcpyAsync(dlist.get(), res.list.data(), nre * 4, cudaMemcpyHostToDevice, st));
   MIHG_CUDA(cudaMemsetAsync(ws.bufcnt.get(), 0, nq * 4, st));
   ProbeArgs rp = p;
+  rp.d_nact = nullptr;  // host-planned: the re-run list size is known
   rp.hist = nullptr;
   rp.trc = nullptr;
   rp.ubound = ws.final_r.get();
@@ -1013,8 +1093,9 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   extract_all_keys(idx, d_q, nq, ws.qsub.get(), st);
   MIHG_CUDA(cudaMemsetAsync(ws.hist.get(), 0, nq * b1 * 4, st));
   MIHG_CUDA(cudaMemsetAsync(ws.trc.get(), 0, 2 * nq * 8, st));
+  MIHG_CUDA(cudaMemsetAsync(ws.nact_dev.get(), 0, ws.nact_dev.size() * 4, st));
   mih_init_kernel<<<g1, 256, 0, st>>>(nq, idx.bits, ws.ubound.get(), ws.bufcnt.get(),
-                                       ws.dropmin.get(), ws.act0.get(), ws.final_r.get());
+                                       ws.dropmin.get(), ws.act0.get(), ws.final_r.get(), ws.nact_dev.get());
   MIHG_LAUNCH();
 
   ProbeArgs p = make_probe_args(idx, ws, d_q);
@@ -1045,31 +1126,61 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   }
 
   std::vector<uint64_t> lookups_prefix;
-  uint32_t* act_in = ws.act0.get();
-  uint32_t* act_out = ws.act1.get();
-  uint64_t nact = nq;
+  // Radius rounds, planned on the device: round r reads its active count from nact_dev[r] and
+  // its end kernel writes nact_dev[r + 1]; the host enqueues rounds ahead of the GPU and learns
+  // the counts from a pinned mirror up to kRunAhead rounds late, so the stream never drains
+  // between rounds. Rounds enqueued after the last query stopped see a count of 0 and exit at
+  // once. nact_known (the newest count read back) bounds the current count from above (counts
+  // never grow): it sizes grids and the slicing decision.
+  constexpr uint32_t kRunAhead = 2;
+  uint32_t* act_buf[2] = {ws.act0.get(), ws.act1.get()};
+  uint64_t nact_known = nq;
+  uint32_t r_known = 0;  // nact_known == nact entering round r_known
   uint64_t acc = 0;
   const double alpha = (d_tr || (part && part->id_shards) || !hybrid_ok) ? 0.0 : hybrid_alpha();
   const double scan_pairs = double(idx.n) * scan_cost_per_code(idx.bits),
                probe_pairs = 36.0 + 15.0 * (idx.W - 1);
   uint32_t* switched = nullptr;
   uint64_t nswitched = 0;
-  for (uint32_t r = 0; nact > 0; ++r) {
+  ProfileState& profst = profile();
+  std::vector<uint32_t> probed_rounds;
+  // read back round `upto`'s end (the count entering round upto + 1), blocking on its event
+  auto learn = [&](uint32_t upto) {
+    while (r_known <= upto) {
+      MIHG_CUDA(cudaEventSynchronize(ws.ev_round[r_known]));
+      nact_known = ws.h_nact[r_known + 1];
+      ++r_known;
+      if (nact_known == 0) return;
+    }
+  };
+  uint32_t r = 0;
+  for (; nact_known > 0; ++r) {
     if (r > idx.bits) throw CudaError("knn: radius loop exceeded the code width (internal error)");
     const uint32_t a = r % m, rr = r / m;
     const uint32_t s = idx.lengths[a];
     const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
-    // the scan of a switched batch costs whole 128-query tiles on the tensor cores (K7), so a few
-    // stragglers are charged a full tile's pass over the database
-    const double scan_q = scan_kernel_for(idx.bits) == ScanKernel::Tensor ? double((nact + 127) / 128 * 128)
-                                                                           : double(nact);
-    if (alpha > 0 && double(acc + ring) * probe_pairs * double(nact) >= alpha * scan_pairs * scan_q) {
-      switched = act_in;  // every active query has probed the same `acc` buckets so far
-      nswitched = nact;
-      neutralise_kernel<<<unsigned(std::min<uint64_t>((nact + 255) / 256, 1024)), 256, 0, st>>>(
-          act_in, uint32_t(nact), ws.final_r.get(), ws.bufcnt.get(), ws.dropmin.get());
-      MIHG_LAUNCH();
-      break;
+    uint32_t* act_in = act_buf[r & 1];
+    uint32_t* act_out = act_buf[(r + 1) & 1];
+    if (alpha > 0) {
+      // the scan of a switched batch costs whole 128-query tiles on the tensor cores (K7), so a few
+      // stragglers are charged a full tile's pass over the database
+      auto wants_switch = [&](uint64_t nact) {
+        const double scan_q = scan_kernel_for(idx.bits) == ScanKernel::Tensor ? double((nact + 127) / 128 * 128)
+                                                                               : double(nact);
+        return double(acc + ring) * probe_pairs * double(nact) >= alpha * scan_pairs * scan_q;
+      };
+      if (wants_switch(nact_known)) {  // decide on the exact count entering round r
+        if (r > 0) learn(r - 1);
+        if (nact_known == 0) break;
+        if (wants_switch(nact_known)) {
+          switched = act_in;  // every active query has probed the same `acc` buckets so far
+          nswitched = nact_known;
+          neutralise_kernel<<<unsigned(std::min<uint64_t>((nswitched + 255) / 256, 1024)), 256, 0, st>>>(
+              act_in, uint32_t(nswitched), ws.final_r.get(), ws.bufcnt.get(), ws.dropmin.get());
+          MIHG_LAUNCH();
+          break;
+        }
+      }
     }
     acc += ring;
     lookups_prefix.push_back(acc);
@@ -1080,12 +1191,16 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
       p.r = r;
       p.active = act_in;
       p.ring = ring;
-      plan_round(p, nact);
-      plan_slicing(p, ws, nact, st);
-      ProfileState& prof = profile();
-      if (prof.enabled) MIHG_CUDA(cudaEventRecord(ws.ev0, st));
+      p.d_nact = ws.nact_dev.get() + r;
+      p.d_chunk = ws.counters.get() + 1;
+      plan_round(p, nact_known);
+      plan_slicing(p, ws, nact_known, st);
+      if (profst.enabled) MIHG_CUDA(cudaEventRecord(ws.ev_probe[2 * r], st));
       dispatch_probe(p, d_tr != nullptr, st);
-      if (prof.enabled) MIHG_CUDA(cudaEventRecord(ws.ev1, st));
+      if (profst.enabled) {
+        MIHG_CUDA(cudaEventRecord(ws.ev_probe[2 * r + 1], st));
+        probed_rounds.push_back(r);
+      }
     }
     const uint32_t* hist_end = ws.hist.get();
     if (part) {  // global histograms: every rank takes the same stopping / bound decision
@@ -1093,20 +1208,28 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
       call_allreduce(part, ws.hist_g.get(), nq * b1, 0, st);
       hist_end = ws.hist_g.get();
     }
-    MIHG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 4, st));
-    const unsigned g = unsigned((nact * 32 + 255) / 256);
-    mih_round_end_kernel<<<g, 256, 0, st>>>(act_in, uint32_t(nact), act_out, ws.counters.get(),
-                                             hist_end, b1, ws.ubound.get(), kstop, r,
+    const unsigned g = unsigned((nact_known * 32 + 255) / 256);
+    mih_round_end_kernel<<<g, 256, 0, st>>>(act_in, uint32_t(nact_known), ws.nact_dev.get() + r, act_out,
+                                             ws.nact_dev.get() + r + 1, hist_end, b1, ws.ubound.get(), kstop, r,
                                              ws.final_r.get(), ws.bufcnt.get(), ws.buf.get(), cap);
     MIHG_LAUNCH();
-    nact = read_counter(ws.counters.get(), ws.h_counter, st);  // synchronizes the stream
-    if (ring && profile().enabled) {
-      float ms = 0;
-      MIHG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
-      profile().probe_ms += ms;
-      profile().probe_launches += 1;
+    MIHG_CUDA(cudaMemcpyAsync(ws.h_nact + r + 1, ws.nact_dev.get() + r + 1, 4, cudaMemcpyDeviceToHost, st));
+    MIHG_CUDA(cudaEventRecord(ws.ev_round[r], st));
+    // keep at most kRunAhead rounds unread; read any that already finished
+    while (r_known <= r && (r + 1 - r_known > kRunAhead || cudaEventQuery(ws.ev_round[r_known]) == cudaSuccess)) {
+      learn(r_known);
+      if (nact_known == 0) break;
     }
-    std::swap(act_in, act_out);
+    if (r == idx.bits && nact_known > 0) learn(r);  // the last possible round: drain
+  }
+  if (profst.enabled) {
+    for (uint32_t pr : probed_rounds) {
+      float ms = 0;
+      MIHG_CUDA(cudaEventSynchronize(ws.ev_probe[2 * pr + 1]));
+      MIHG_CUDA(cudaEventElapsedTime(&ms, ws.ev_probe[2 * pr], ws.ev_probe[2 * pr + 1]));
+      profst.probe_ms += ms;
+      profst.probe_launches += 1;
+    }
   }
   MIHG_CUDA(cudaMemcpyAsync(ws.lookups_prefix.get(), lookups_prefix.data(),
                             lookups_prefix.size() * 8, cudaMemcpyHostToDevice, st));

@@ -132,19 +132,24 @@ constexpr uint32_t tc_idesc(uint32_t M, uint32_t N) {
   return (2u << 4) | (1u << 7) | (0u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-#define TC_R8(i) "=r"(v[i + 0]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), \
-                 "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
-// 32 TMEM lanes x 32 consecutive 32-bit columns -> 32 registers per thread (lane = thread).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+
+#define TC_R8U(i) "=r"(v[i + 0]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), \
+                  "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+// 32 TMEM lanes x 64 consecutive 32-bit columns -> 32 registers per thread, each holding the low
+// 16 bits of two adjacent columns (column 2i in bits 0-15, 2i+1 in bits 16-31; measured layout,
+// tools/probe/tmem_ld.cu). The accumulators are d(q, x) - popc(q) in [-256, 256], exact in 16
+// bits; the packed load moves half the register bytes: 64 columns x 16 warps in 162 clk vs 408
+// clk for two plain .x32 loads (B200, same probe), and the minimum tree runs on halfword pairs.
+__device__ __forceinline__ void tmem_ld64_pack16(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : TC_R8(0), TC_R8(8), TC_R8(16), TC_R8(24)
+      : TC_R8U(0), TC_R8U(8), TC_R8U(16), TC_R8U(24)
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-#undef TC_R8
+#undef TC_R8U
 
 // 4 bits -> 4 bytes of 0/1 (bit i -> byte i)
 __device__ __forceinline__ uint32_t spread4(uint32_t x) { return (x * 0x00204081u) & 0x01010101u; }
@@ -426,37 +431,42 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         }
         wait_k(tfull + b, (t / kAcc) & 1, 0);  // the tile's MMAs are complete
         tc_fence_after();
-#pragma unroll 1
-        for (int sc = 0; sc < kEpiCols / 32; ++sc) {  // 32-column sub-chunks of this group's columns
-        int32_t v[32];
-        tmem_ld32(taddr0 + b * kTcN + sc * 32, v);
-        if (sc == kEpiCols / 32 - 1) {
-          tc_fence_before();  // accumulator drained into registers: hand it back
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty + b);
-        }
-        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols + sc * 32;
+        static_assert(kEpiCols == 64, "packed epilogue drains 64 columns per group");
+        {
+        uint32_t v[32];
+        tmem_ld64_pack16(taddr0 + b * kTcN, v);
+        tc_fence_before();  // accumulator drained into registers: hand it back
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + b);
+        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols;
         if constexpr (kDump) {
           if (qvalid)
-            for (int j = 0; j < 32; ++j)
-              if (id0 + j < hi) a.dump[q * a.n + id0 + j] = v[j] + pq;
+            for (int j = 0; j < 64; ++j) {
+              const int32_t x = int32_t(int16_t(uint16_t(v[j >> 1] >> ((j & 1) * 16))));
+              if (id0 + j < hi) a.dump[q * a.n + id0 + j] = x + pq;
+            }
         }
         const int32_t thr = min(own, shared_b) - pq;
-        // tree minimum (independent 3-input mins, short dependency chain)
-        int32_t m8[11];
+        // halfword-SIMD tree minimum over the 64 packed values
+        uint32_t m16[16];
 #pragma unroll
-        for (int i = 0; i < 10; ++i) m8[i] = min(min(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
-        m8[10] = min(v[30], v[31]);
-        const int32_t m3a = min(min(m8[0], m8[1]), m8[2]), m3b = min(min(m8[3], m8[4]), m8[5]);
-        const int32_t m3c = min(min(m8[6], m8[7]), m8[8]), m3d = min(m8[9], m8[10]);
-        const bool any_hit = min(min(m3a, m3b), min(m3c, m3d)) <= thr;
-        if (any_hit) {
-          // hit mask, then the (few) hits re-derive their distance from the code words (L2-hot)
-          uint32_t m = 0;
+        for (int i = 0; i < 16; ++i) m16[i] = __vmins2(v[2 * i], v[2 * i + 1]);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) m |= uint32_t(v[j] <= thr) << j;
+        for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+          for (int i = 0; i < w; ++i) m16[i] = __vmins2(m16[i], m16[i + w]);
+        const int32_t mn = min(int32_t(int16_t(uint16_t(m16[0]))), int32_t(int16_t(uint16_t(m16[0] >> 16))));
+        if (mn <= thr) {
+          // hit mask (two bits per register), then the (few) hits re-derive their distance
+          const uint32_t t2 = uint32_t(uint16_t(int16_t(thr))) * 0x00010001u;
+          uint64_t m = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const uint32_t le = __vcmples2(v[i], t2);  // 0xFFFF per halfword <= thr
+            m |= uint64_t((le & 1u) | ((le >> 15) & 2u)) << (2 * i);
+          }
           while (m) {
-            const uint32_t j = __ffs(m) - 1;
+            const uint32_t j = __ffsll(static_cast<long long>(m)) - 1;
             m &= m - 1;
             const uint64_t id = id0 + j;
             if (id >= hi) break;
@@ -482,7 +492,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           }
           __syncwarp();
         }
-        }  // sub-chunks
+        }
       }
       if (qvalid) a.counts[q * a.slots + slot] = cnt;
     }

@@ -36,6 +36,21 @@ def knn_case(R, codes, bits, m, queries, ks, lengths=None, positions=None):
     return out
 
 
+def clustered_codes(n, bits, centers, flips, seed):
+    """Codes within a few bit flips of random centres (numpy PCG64, stored in the fixture): exact
+    kNN radii stay small at any width, so the reference MIH answers wide codes quickly."""
+    rng = np.random.default_rng(seed)
+    W = (bits + 63) // 64
+    cen = rng.integers(0, 2**64, size=(centers, W), dtype=np.uint64)
+    out = cen[rng.integers(0, centers, size=n)].copy()
+    for i in range(n):
+        for pos in rng.choice(bits, size=int(rng.integers(0, flips + 1)), replace=False):
+            out[i, pos // 64] ^= np.uint64(1) << np.uint64(pos % 64)
+    if bits % 64:
+        out[:, -1] &= np.uint64((1 << (bits % 64)) - 1)
+    return out
+
+
 def digest(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -123,6 +138,8 @@ def main(only=None):
     if only == "optimize":
         files = {"optimize": files["optimize"]}
         return save(files)
+    if only == "wide":
+        files = {}
 
     # index_test.cpp:73-94 HandWorkedKnn (and scan_test.cpp:14-19 tiny_db)
     codes = np.array([[0], [1], [63]], np.uint64)
@@ -299,12 +316,29 @@ def main(only=None):
         case += 1
     files["bmix_files"] = bm
 
+    # Codes wider than 256 bits (codes.hpp:16 allows up to 4096): the GPU's generic-width paths.
+    # 300 bits (W = 5, a partial last word), m = 10 x 30-bit substrings; 512 bits (W = 8), m = 16
+    # x 32-bit substrings (sparse tables). Clustered codes, queries near the centres; the
+    # reference's MIH (ids, dists, traces) and scan_knn (scan.hpp:43-68) answers.
+    for bits, m, seed in ((300, 10, 300), (512, 16, 512)):
+        codes = clustered_codes(2000, bits, 40, 12, seed)
+        qs = clustered_codes(12, bits, 40, 12, seed)  # same centres (same seed), other flips
+        qs = np.concatenate([qs, R.gen_uniform(2, bits, seed + 1)])  # and two far-away queries
+        d = dict(bits=bits, m=m, codes=codes, queries=qs[:12], scan_queries=qs,
+                 **knn_case(R, codes, bits, m, qs[:12], [1, 10, 40]))
+        for k in (1, 10, 60):
+            si, sd = R.scan_knn(codes, bits, qs, k)
+            d[f"scan_ids_k{k}"], d[f"scan_dists_k{k}"] = si, sd
+        files[f"wide{bits}"] = d
+
     # gen_uniform pins (io.hpp:266-277): several widths and seeds.
     pins = {}
     for n, bits, seed in ((5, 64, 1), (7, 70, 181), (3, 256, 42), (4, 24, 501), (2, 130, 9)):
         pins[f"gen_{n}_{bits}_{seed}"] = R.gen_uniform(n, bits, seed)
     files["gen_uniform_pins"] = pins
 
+    if only == "wide":
+        files = {k: v for k, v in files.items() if k.startswith("wide")}
     save(files)
 
 

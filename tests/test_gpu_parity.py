@@ -34,7 +34,18 @@ def _index(d, layout="auto"):
 
 
 CASES = ["hand_worked", "knn_wide24", "duplicates", "self_queries", "nondivisible100",
-         "scratch_reuse32", "lsh_io_test", "interleaved64", "acceptance_lsh"]
+         "scratch_reuse32", "lsh_io_test", "interleaved64", "acceptance_lsh", "wide300", "wide512"]
+
+
+@pytest.mark.parametrize("bits", [300, 512])
+def test_scan_wide_matches_reference_golden(cuda_ok, golden, bits):
+    """Codes above 256 bits (codes.hpp:16): generic-width K6 scan vs the reference's scan_knn."""
+    mg = _mg()
+    d = golden(f"wide{bits}")
+    idx = mg.MihIndex.build(mg.CodeDatabase(bits, d["codes"]), mg.consecutive_partition(bits, int(d["m"])))
+    for k in (1, 10, 60):
+        ids, dists = idx.scan_knn_batch(d["scan_queries"], k)
+        assert np.array_equal(ids, d[f"scan_ids_k{k}"]) and np.array_equal(dists, d[f"scan_dists_k{k}"]), k
 
 
 @pytest.mark.parametrize("layout", ["auto", "sparse"])

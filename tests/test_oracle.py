@@ -13,6 +13,8 @@ KNN_CASES = [
     ("lsh_io_test", None),
     ("interleaved64", None),
     ("acceptance_lsh", None),
+    ("wide300", None),
+    ("wide512", None),
 ]
 
 
@@ -45,6 +47,14 @@ def test_port_knn_random_matches_reference(port, golden, bits):
             assert np.array_equal(ids, d[f"m{m}_ids_k{k}"])
             assert np.array_equal(dists, d[f"m{m}_dists_k{k}"])
             assert np.array_equal(tr, d[f"m{m}_trace_k{k}"])
+
+
+@pytest.mark.parametrize("bits", [300, 512])
+def test_port_scan_wide_matches_reference(port, golden, bits):
+    d = golden(f"wide{bits}")
+    for k in (1, 10, 60):
+        ids, dists = port.scan_knn(d["codes"], bits, d["scan_queries"], k)
+        assert np.array_equal(ids, d[f"scan_ids_k{k}"]) and np.array_equal(dists, d[f"scan_dists_k{k}"])
 
 
 def test_port_scan_matches_reference(port, golden):

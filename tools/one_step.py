@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--nq", type=int, default=0)
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--traced", action="store_true")
+    ap.add_argument("--profile-search", action="store_true",
+                    help="bracket only the search with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     a = ap.parse_args()
     import torch
 
@@ -40,8 +42,14 @@ def main():
     ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
     d = torch.empty((nq, k), dtype=torch.int32, device=dev)
     tr = torch.empty((nq, 5), dtype=torch.int64, device=dev) if a.traced else None
+    if a.profile_search:  # warm-up search outside the profiled range
+        idx.knn_search_device(qs.data_ptr(), nq, k, ids.data_ptr(), d.data_ptr(), None)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
     idx.knn_search_device(qs.data_ptr(), nq, k, ids.data_ptr(), d.data_ptr(), tr.data_ptr() if a.traced else None)
     torch.cuda.synchronize()
+    if a.profile_search:
+        torch.cuda.profiler.stop()
     if a.traced:
         t = tr.cpu().numpy().astype(np.float64)
         alg = float((8 * t[:, 0] + 4 * t[:, 1] + (cfg["bits"] / 8) * t[:, 2]).sum())

@@ -185,9 +185,13 @@ def config_desc(cfg, args, world):
                      f"{cfg['bits']}-bit {cfg['data']} codes, {cfg['nq']} queries, MIH m={cfg['m']}",
          "n": cfg["n"], "bits": cfg["bits"], "m": cfg["m"], "k": cfg["k"], "queries": cfg["nq"],
          "data_generator": cfg["data"],
-         "parallelism": (f"probe-space partition x{world} (replicated index, 1/{world} of the key space "
-                         f"per rank, per-round NCCL histogram all-reduce)" if world > 1 and args.shard == "probe"
-                         else f"id-range shards x{world}"),
+         "parallelism": (f"probe-space partition x{world} (replicated index, rank g probes the ring values whose "
+                         f"top log2({world}) key bits equal g; per-round NCCL histogram all-reduce, NCCL all-gather "
+                         f"of local top-k + device merge, all inside libmihg)" if world > 1 and args.shard == "probe"
+                         else (f"id-range shards x{world} (north_star layout: rank g indexes ids [g*ceil(n/{world}), ...); "
+                               f"global stopping via per-round NCCL histogram all-reduce; NCCL all-gather + device "
+                               f"merge, all inside libmihg)" if world > 1 else "single GPU")),
+         "allgather_bytes_per_step": int(world * cfg["nq"] * cfg["k"] * 8) if world > 1 else 0,
          "l2_policy": "inputs larger than L2 (index >> 126 MB); no flush"}
     if cfg["data"] == "mixture":
         d.update({"mixture": {"dim": MIX_DIM, "components": MIX_COMPS, "sigma_rel": 1.0,
@@ -416,23 +420,30 @@ def main():
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
 
-    partition = None
-    if probe_part:
-        from paper_1307_2982_b200.shard import nccl_allreduce
+    # N > 1, MIH: one library call per rank and step (mihg_knn_sharded_device): the per-round NCCL
+    # histogram all-reduce, the NCCL all-gather of the local top-k lists and the exact device merge
+    # all run inside libmihg on its own NCCL communicator (no host language in the round loop)
+    comm = None
+    layout = 0 if probe_part else 1
+    if use_dist and args.method == "mih":
+        from paper_1307_2982_b200.shard import NcclComm
 
-        partition = (world, rank, nccl_allreduce())
-    elif world > 1 and args.method == "mih":  # id-range shards with global stopping (§8e refinement 1)
-        from paper_1307_2982_b200.shard import nccl_allreduce
+        comm = NcclComm(local_rank)
 
-        partition = (world, rank, nccl_allreduce(), True, k)  # stopping rule on the global k
+    def sharded(qptr, nqq, out_i, out_dd, trp=None):
+        _lib.check(L.mihg_knn_sharded_device(idx._h, comm.handle, layout, cfg["n"], C.c_void_p(qptr), nqq, k,
+                                             C.c_void_p(out_i.data_ptr()), C.c_void_p(out_dd.data_ptr()),
+                                             C.c_void_p(trp) if trp else None, C.c_void_p(stream.cuda_stream)))
 
     def step(qptr=None):
         qptr = qptr or queries.data_ptr()
+        if comm is not None:
+            sharded(qptr, nq, out_ids, out_d)
+            return
         if args.method == "scan":
             idx.scan_knn_device(qptr, nq, kk, ids.data_ptr(), dists.data_ptr(), stream=stream.cuda_stream)
         else:
-            idx.knn_search_device(qptr, nq, kk, ids.data_ptr(), dists.data_ptr(),
-                                  stream=stream.cuda_stream, partition=partition)
+            idx.knn_search_device(qptr, nq, kk, ids.data_ptr(), dists.data_ptr(), stream=stream.cuda_stream)
         if use_dist:
             dist.all_gather_into_tensor(all_ids, ids)
             dist.all_gather_into_tensor(all_d, dists)
@@ -524,8 +535,11 @@ def main():
     # scaled: its numbers only feed the HBM roofline, which the hybrid's tensor-core line replaces)
     nq_tr = nq if bits <= 128 else min(nq, 256)
     tr = torch.empty((nq_tr, 5), dtype=torch.int64, device=dev)
-    idx.knn_search_device(queries.data_ptr(), nq_tr, kk, ids.data_ptr(), dists.data_ptr(), tr.data_ptr(),
-                          stream=stream.cuda_stream, partition=partition)
+    if comm is not None:  # global traces (candidates / unique summed over ranks)
+        sharded(queries.data_ptr(), nq_tr, torch.empty_like(out_ids), torch.empty_like(out_d), tr.data_ptr())
+    else:
+        idx.knn_search_device(queries.data_ptr(), nq_tr, kk, ids.data_ptr(), dists.data_ptr(), tr.data_ptr(),
+                              stream=stream.cuda_stream)
     torch.cuda.synchronize(dev)
     t = tr.cpu().numpy()
     lookups, cands, uniq, radius = (t[:, 0].astype(np.float64), t[:, 1].astype(np.float64),

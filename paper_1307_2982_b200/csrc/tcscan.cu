@@ -109,6 +109,59 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+// ---- CTA-pair (cta_group::2) helpers ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// (the CUTLASS 2x1SM pattern: default .release.cta semantics; the operand bytes reach the tensor
+// core through the async proxy, ordered by the writer's fence.proxy.async)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// wait with cluster-scope acquire (arrivals come from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the issued MMAs complete
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+// D[tmem, both SMs] (+)= A[smem, 128 rows per CTA] . B[smem, N/2 rows per CTA]^T, kind::i8, M = 256
+__device__ __forceinline__ void tc_mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // D[tmem] (+)= A[smem] . B[smem]^T, kind::i8 (A signed, B unsigned, s32 accumulate)
 __device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -168,32 +221,37 @@ __device__ __forceinline__ uint32_t kstep_addr(uint32_t base, int kk, uint32_t r
 // The 16-byte-aligned part of a raw tile's code bytes (TMA bulk copies need 16-byte alignment and
 // size): it starts `skip` bytes into the tile and is `bytes` long; codes outside it (a misaligned
 // head, an odd tail) are read with plain loads.
-template <int W>
+template <int W, int kCodes>
 __device__ __forceinline__ void raw_span(const uint64_t* codes, uint64_t id0, uint64_t hi, uint32_t& skip,
                                          uint32_t& bytes) {
-  const uintptr_t s = reinterpret_cast<uintptr_t>(codes + id0 * W);
-  const uintptr_t e = reinterpret_cast<uintptr_t>(codes + min(hi, id0 + kTcN) * W);
+  const uintptr_t s = reinterpret_cast<uintptr_t>(codes + min(hi, id0) * W);
+  const uintptr_t e = reinterpret_cast<uintptr_t>(codes + min(hi, id0 + kCodes) * W);
   const uintptr_t s16 = (s + 15) & ~uintptr_t(15), e16 = e & ~uintptr_t(15);
   skip = uint32_t(s16 - s);
   bytes = e16 > s16 ? uint32_t(e16 - s16) : 0u;
 }
 
-template <int KB>
+// kPair: a CTA pair (cluster of 2, cta_group::2) shares each 256-code tile: M = 256 queries (128
+// rows of A per CTA), each CTA expands and holds N/2 = 128 codes of B, and each SM's TMEM receives
+// its 128 query rows x all 256 codes. Per SM, the expansion and the B operand bytes halve.
+template <int KB, bool kPair = false>
 struct TcCfg {
   static constexpr int W = KB / 64;
   static constexpr uint32_t kOpBytes = KB;
   static constexpr int kSteps = kOpBytes / 32;
   static constexpr uint32_t kKBp = (kOpBytes + 127) / 128 * 128;  // whole 128-byte swizzle rows
+  static constexpr int kCodes = kPair ? kTcN / 2 : kTcN;           // codes per CTA per tile
   static constexpr uint32_t kA = kTcM * kKBp;  // A (queries) in shared memory
-  static constexpr uint32_t kB = kTcN * kKBp;
-  static constexpr int kStages = kKBp <= 128 ? 4 : 2;
-  static constexpr uint32_t kRawBytes = kTcN * W * 8;  // one raw tile of packed codes
+  static constexpr uint32_t kB = kCodes * kKBp;
+  static constexpr int kStages = (kKBp <= 128 ? 4 : 2) * (kPair ? 2 : 1);
+  static constexpr uint32_t kRawBytes = kCodes * W * 8;  // one raw tile of packed codes
   static constexpr uint32_t kSmem = 1024 + kA + kStages * kB + kRaw * kRawBytes;  // + barriers/hist
 };
 
-template <int KB, bool kDump>
+template <int KB, bool kDump, bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
-  using Cfg = TcCfg<KB>;
+  using Cfg = TcCfg<KB, kPair>;
+  constexpr int kCodes = Cfg::kCodes;
   constexpr int W = Cfg::W;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -224,15 +282,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   auto wait_k = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
 #endif
 
+  const uint32_t rank = kPair ? cluster_rank() : 0u;  // 0: the pair's MMA issuer
+  constexpr uint32_t kSides = kPair ? 2 : 1;
   if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) {
-        mbar_init(full + s, kProdWarps);
+        mbar_init(full + s, kProdWarps * kSides);  // (pair: used in rank 0 only)
         mbar_init(empty + s, 1);
       }
       for (int b = 0; b < kAcc; ++b) {
         mbar_init(tfull + b, 1);
-        mbar_init(tempty + b, kEpiWarps);
+        mbar_init(tempty + b, kEpiWarps * kSides);  // (pair: used in rank 0 only)
       }
       for (int r = 0; r < kRaw; ++r) {
         mbar_init(rfull + r, 1);
@@ -241,18 +301,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kPair) {  // both CTAs' MMA warps (same warp id) allocate the pair's TMEM
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // pair: producers and epilogues report to rank 0's full / tempty barriers
+  const uint32_t full_c = kPair ? mapa(smem_u32(full), 0) : 0u;
+  const uint32_t tempty_c = kPair ? mapa(smem_u32(tempty), 0) : 0u;
 
   // This CTA's work items [i0, i1) (tile-major): consecutive items of one query tile form a
   // segment over one contiguous id range, with one candidate list per (query, group).
+  // work unit: one CTA, or one CTA pair (both CTAs walk the same items)
+  const uint32_t unit = kPair ? blockIdx.x / 2 : blockIdx.x;
   const uint64_t items = uint64_t(a.qtiles) * a.nch;
-  const uint64_t i0 = uint64_t(blockIdx.x) * a.ipc, i1 = min(items, i0 + a.ipc);
+  const uint64_t i0 = uint64_t(unit) * a.ipc, i1 = min(items, i0 + a.ipc);
   uint32_t tg = 0;  // tiles processed by this CTA so far: drives every pipeline phase
 #ifdef MIHG_TC_DEBUG
   uint32_t mo_phase = 0;  // mma_only probe
@@ -264,8 +335,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     const uint64_t lo = (it - uint64_t(Q) * a.nch) * a.chunk;
     const uint64_t hi = min(a.n, (it_end - uint64_t(Q) * a.nch) * a.chunk);
     const uint32_t T = uint32_t((hi - lo + kTcN - 1) / kTcN);
-    const uint32_t slot0 = (blockIdx.x - uint32_t((uint64_t(Q) * a.nch) / a.ipc)) * kEpiGroups;
-    const uint64_t q0 = uint64_t(Q) * kTcM;
+    const uint32_t slot0 = (unit - uint32_t((uint64_t(Q) * a.nch) / a.ipc)) * kEpiGroups;
+    const uint64_t q0 = uint64_t(Q) * kTcM * kSides + rank * kTcM;  // this CTA's 128 query rows
     it = it_end;
 
     // A operand in shared memory (128B-swizzled K-major, like B): row r = query q0 + r as K bytes
@@ -288,11 +359,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     }
     fence_proxy_async();
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) cluster_sync();  // both halves of A written before the pair's MMAs
+    else __syncthreads();
     tc_fence_after();
 
 #ifdef MIHG_TC_DEBUG
-    if (a.mma_only) {
+    if (!kPair && a.mma_only) {
       if (warp == kMmaWarp && lane == 0) {
         constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
         const uint32_t b_addr = smem_u32(sB);
@@ -311,22 +383,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     } else
 #endif
     if (warp == kMmaWarp) {
-      // ===== MMA issuer =====
-      if (lane == 0) {
-        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
+      // ===== MMA issuer (pair: rank 0 only, for both SMs) =====
+      if (lane == 0 && rank == 0) {
+        constexpr uint32_t idesc = tc_idesc(kTcM * kSides, kTcN);
         const uint32_t b_addr = smem_u32(sB);
         for (uint32_t t = tg; t < tg + T; ++t) {
           const uint32_t s = t % S, ph = (t / S) & 1, b = t % kAcc, bph = (t / kAcc) & 1;
-          wait_k(tempty + b, bph ^ 1, 0);
-          wait_k(full + s, ph, 1);
+          if constexpr (kPair) {
+            mbar_wait_cluster(tempty + b, bph ^ 1);
+            mbar_wait_cluster(full + s, ph);
+          } else {
+            wait_k(tempty + b, bph ^ 1, 0);
+            wait_k(full + s, ph, 1);
+          }
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < Cfg::kSteps; ++kk) {  // 32 bytes = 8 TMEM columns of A per step
-            const uint64_t bd = smem_desc_sw128(kstep_addr(b_addr + s * Cfg::kB, kk, kTcN));
-            tc_mma_i8(tmem + b * kTcN, smem_desc_sw128(kstep_addr(smem_u32(sA), kk, kTcM)), bd, idesc, kk > 0);
+          for (int kk = 0; kk < Cfg::kSteps; ++kk) {  // 32 bytes of K per step
+            const uint64_t bd = smem_desc_sw128(kstep_addr(b_addr + s * Cfg::kB, kk, kCodes));
+            const uint64_t ad = smem_desc_sw128(kstep_addr(smem_u32(sA), kk, kTcM));
+            if constexpr (kPair) tc_mma_i8_pair(tmem + b * kTcN, ad, bd, idesc, kk > 0);
+            else tc_mma_i8(tmem + b * kTcN, ad, bd, idesc, kk > 0);
           }
-          tc_commit(empty + s);  // frees the B stage
-          tc_commit(tfull + b);  // publishes the accumulator
+          if constexpr (kPair) {
+            tc_commit_pair(empty + s);  // frees the B stage in both CTAs
+            tc_commit_pair(tfull + b);  // publishes the accumulator in both SMs
+          } else {
+            tc_commit(empty + s);
+            tc_commit(tfull + b);
+          }
         }
       }
       __syncwarp();
@@ -336,9 +420,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         for (uint32_t t = tg; t < tg + T; ++t) {
           const uint32_t r = t % kRaw;
           wait_k(rempty + r, ((t / kRaw) & 1) ^ 1, 0);
-          const uint64_t id0 = lo + uint64_t(t - tg) * kTcN;
+          const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + rank * kCodes;  // this CTA's codes
           uint32_t skip, bytes;
-          raw_span<W>(a.codes, id0, hi, skip, bytes);
+          raw_span<W, kCodes>(a.codes, id0, hi, skip, bytes);
           const uint32_t bar = smem_u32(rfull + r);
           if (bytes) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -354,17 +438,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
       }
       __syncwarp();
     } else if (warp >= kEpiWarps) {
-      // ===== producers: raw code -> 0/1 bytes (kTcN / 128 codes per thread per tile) =====
+      // ===== producers: raw code -> 0/1 bytes (kCodes / 128 codes per thread per tile) =====
       const uint32_t p0 = threadIdx.x - kEpiWarps * 32;
       for (uint32_t t = tg; t < tg + T; ++t) {
         const uint32_t s = t % S, ph = (t / S) & 1, r = t % kRaw;
-        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN;
+        const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + rank * kCodes;
         uint32_t skip, tbytes;
-        raw_span<W>(a.codes, id0, hi, skip, tbytes);
+        raw_span<W, kCodes>(a.codes, id0, hi, skip, tbytes);
         wait_k(rfull + r, (t / kRaw) & 1, 0);
-        uint64_t cur[kTcN / 128][W];
+        uint64_t cur[kCodes / 128][W];
 #pragma unroll
-        for (int h = 0; h < kTcN / 128; ++h) {
+        for (int h = 0; h < kCodes / 128; ++h) {
           const uint32_t p = p0 + 128 * h;
           const uint64_t id = id0 + p;
           if (p * W * 8 >= skip && (p + 1) * W * 8 <= skip + tbytes) {
@@ -382,20 +466,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         wait_k(empty + s, ph ^ 1, 1);
         uint8_t* dst = sB + s * Cfg::kB;
 #pragma unroll
-        for (int h = 0; h < kTcN / 128; ++h) {
+        for (int h = 0; h < kCodes / 128; ++h) {
           const uint32_t p = p0 + 128 * h;
 #pragma unroll
           for (int c = 0; c < KB / 16; ++c) {
             const uint32_t hh = uint32_t(cur[h][c >> 2] >> ((c & 3) * 16)) & 0xFFFFu;
             const uint4 o = make_uint4(spread4(hh & 0xF), spread4((hh >> 4) & 0xF), spread4((hh >> 8) & 0xF),
                                        spread4(hh >> 12));
-            *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c, kTcN)) = o;
+            *reinterpret_cast<uint4*>(dst + core_off<KB>(p, c, kCodes)) = o;
           }
         }
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(full + s);
+          if constexpr (kPair) mbar_arrive_cluster(full_c + s * 8);  // rank 0's barrier
+          else mbar_arrive(full + s);
           mbar_arrive(rempty + r);  // the raw words were consumed by the expansion above
         }
       }
@@ -437,7 +522,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         tmem_ld64_pack16(taddr0 + b * kTcN, v);
         tc_fence_before();  // accumulator drained into registers: hand it back
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty + b);
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_cluster(tempty_c + b * 8);  // rank 0's barrier
+          else mbar_arrive(tempty + b);
+        }
         const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols;
         if constexpr (kDump) {
           if (qvalid)
@@ -502,7 +590,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
 #endif
     // segment end: every MMA of the segment was drained by the epilogue, so A may be reloaded
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
   }
 #ifdef MIHG_TC_DEBUG
@@ -513,36 +602,63 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     atomicAdd(pr + 5, (unsigned long long)tiles_total);
   }
 #endif
-  if (warp == kMmaWarp) {
+  if constexpr (kPair) {
+    tc_fence_before();
+    cluster_sync();  // both SMs done with the pair's TMEM and barriers
+    tc_fence_after();
+    if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  } else if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
-template <int KB>
+template <int KB, bool kPair>
 size_t tc_smem_bytes(uint32_t bits) {
-  using Cfg = TcCfg<KB>;
+  using Cfg = TcCfg<KB, kPair>;
   return Cfg::kSmem + (2 * Cfg::kStages + 2 * kAcc + 2 * kRaw) * 8 + 16 + size_t(kEpiWarps) * (bits + 1) * 4;
 }
 
-template <int KB, bool kDump>
+template <int KB, bool kDump, bool kPair>
 void launch_tc_k(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  const size_t smem = tc_smem_bytes<KB>(a.bits);
-  MIHG_CUDA(cudaFuncSetAttribute(tc_scan_kernel<KB, kDump>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-  tc_scan_kernel<KB, kDump><<<grid, kTcThreads, smem, st>>>(a);
+  const size_t smem = tc_smem_bytes<KB, kPair>(a.bits);
+  auto* fn = tc_scan_kernel<KB, kDump, kPair>;
+  MIHG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if constexpr (kPair) {  // clusters of two CTAs on one TPC
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MIHG_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
+  } else {
+    fn<<<grid, kTcThreads, smem, st>>>(a);
+  }
   MIHG_LAUNCH();
 }
 
-template <int KB>
+template <int KB, bool kPair>
 void launch_tc(const TcArgs& a, uint32_t grid, cudaStream_t st) {
-  if (a.dump) launch_tc_k<KB, true>(a, grid, st);
-  else launch_tc_k<KB, false>(a, grid, st);
+  if (a.dump) launch_tc_k<KB, true, kPair>(a, grid, st);
+  else launch_tc_k<KB, false, kPair>(a, grid, st);
 }
 
 }  // namespace
 
 bool tc_scan_supported(uint32_t bits) { return bits >= 1 && bits <= 256; }
+
+// CTA-pair (cta_group::2) K7: MIHG_TC_PAIR=1|0 selects (default 0 until measured).
+bool tc_pair_enabled() {
+  const char* e = std::getenv("MIHG_TC_PAIR");  // read per call: tests run both geometries
+  return e && e[0] == '1';
+}
 
 // K7: the exhaustive k-NN of scan_knn_device on the tensor cores (same results bit for bit).
 void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
@@ -553,10 +669,12 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
   if (nq == 0 || k == 0) return;
   const uint32_t W = words_per_code(bits);
   const uint32_t L = 2 * k + kEpiCols;
-  const uint64_t sms = uint64_t(device_sm_count());
+  const bool pair = tc_pair_enabled();
+  const uint64_t tileq = pair ? 2 * kTcM : kTcM;  // queries per work unit (CTA or CTA pair)
+  const uint64_t sms = uint64_t(device_sm_count()) / (pair ? 2 : 1);  // work units in flight
   for (uint64_t q0 = 0; q0 < nq;) {
     uint64_t qn = nq - q0;
-    uint64_t qtiles = (qn + kTcM - 1) / kTcM;
+    uint64_t qtiles = (qn + tileq - 1) / tileq;
     // Persistent CTAs, one per SM, each over a contiguous range of (query tile, chunk) items.
     // nch is a multiple of sms / gcd(qtiles, sms) so the items divide evenly over the SMs, with
     // at least 8 items per CTA; chunks of at least 16 tiles.
@@ -577,15 +695,15 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     uint64_t spq = spq_of(qtiles, nch, ipc);
     // list memory bound (~2 GiB): fewer queries per pass when k is large
     const uint64_t per_q = kEpiGroups * spq * uint64_t(L) * 8 * 2;
-    const uint64_t qmax = std::max<uint64_t>(kTcM, (uint64_t(2) << 30) / per_q / kTcM * kTcM);
+    const uint64_t qmax = std::max<uint64_t>(tileq, (uint64_t(2) << 30) / per_q / tileq * tileq);
     if (qn > qmax) {
       qn = qmax;
-      qtiles = qn / kTcM;
+      qtiles = qn / tileq;
       items = qtiles * nch;
       ipc = (items + sms - 1) / sms;
       spq = spq_of(qtiles, nch, ipc);
     }
-    const uint32_t grid = uint32_t((items + ipc - 1) / ipc);
+    const uint32_t grid = uint32_t((items + ipc - 1) / ipc) * (pair ? 2 : 1);
     TcArgs a{};
     a.codes = d_codes;
     a.n = n;
@@ -628,11 +746,20 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
       }
       MIHG_CUDA(cudaEventRecord(ev[0], st));
     }
-    switch (W) {
-      case 1: launch_tc<64>(a, grid, st); break;
-      case 2: launch_tc<128>(a, grid, st); break;
-      case 3: launch_tc<192>(a, grid, st); break;
-      default: launch_tc<256>(a, grid, st); break;
+    if (pair) {
+      switch (W) {
+        case 1: launch_tc<64, true>(a, grid, st); break;
+        case 2: launch_tc<128, true>(a, grid, st); break;
+        case 3: launch_tc<192, true>(a, grid, st); break;
+        default: launch_tc<256, true>(a, grid, st); break;
+      }
+    } else {
+      switch (W) {
+        case 1: launch_tc<64, false>(a, grid, st); break;
+        case 2: launch_tc<128, false>(a, grid, st); break;
+        case 3: launch_tc<192, false>(a, grid, st); break;
+        default: launch_tc<256, false>(a, grid, st); break;
+      }
     }
     if (prof) MIHG_CUDA(cudaEventRecord(ev[1], st));
 #ifdef MIHG_TC_DEBUG

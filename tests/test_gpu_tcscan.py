@@ -10,6 +10,16 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["single", "pair"], autouse=True)
+def tc_geometry(request):
+    """Every K7 test runs in both geometries: one CTA per 128-query x 256-code tile, and CTA pairs
+    (cta_group::2, M = 256) that split each code tile between two SMs (MIHG_TC_PAIR=1)."""
+    if request.param == "pair":
+        os.environ["MIHG_TC_PAIR"] = "1"
+    yield request.param
+    os.environ.pop("MIHG_TC_PAIR", None)
+
+
 def _popc_dist(q, x):
     """[nq, n] Hamming distances of packed u64 rows (numpy restatement of hamming_words)."""
     d = np.zeros((q.shape[0], x.shape[0]), np.int64)

@@ -161,66 +161,78 @@ void finish_correlations(const uint64_t* counts, uint64_t n, uint32_t bits, doub
   }
 }
 
+// greedy_assign (optimize.hpp:101-172), restated as incremental arg-min/arg-max scans. Per
+// substring j the table near[j][c] holds max over j's members o of |corr(c, o)|, raised by one row of
+// the matrix whenever j takes a bit, so a visit is a single pass over the free bits (O(b)) instead
+// of re-reducing over the members. Selection rules are the reference's: strict comparisons over
+// ascending bit index (ties to the lowest index), the chain opening through mt19937_64 +
+// uniform_int_distribution over the free non-constant bits, balanced capacities with the extras
+// on the lowest substrings, constant bits dealt round-robin last, members sorted.
 void greedy_assign(const double* corr, const uint8_t* constant, uint32_t bits, uint32_t m,
                    uint64_t seed, uint32_t* lengths, uint32_t* positions) {
   if (m == 0 || m > bits) throw InvalidArgument("greedy_assign: need 1 <= m <= bits");
-  auto at = [&](uint32_t i, uint32_t j) { return corr[uint64_t(i) * bits + j]; };
-  std::vector<uint32_t> cap(m, bits / m);
-  for (uint32_t j = 0; j < bits % m; ++j) ++cap[j];
-  std::vector<std::vector<uint32_t>> subs(m);
-  std::vector<uint32_t> pool, constants;  // pool: non-constant unassigned bits, ascending
-  for (uint32_t i = 0; i < bits; ++i) (constant[i] ? constants : pool).push_back(i);
-  auto take = [&](uint32_t v) { pool.erase(std::find(pool.begin(), pool.end(), v)); };
+  const auto row = [&](uint32_t i) { return corr + uint64_t(i) * bits; };
+  std::vector<uint32_t> capacity(m);
+  for (uint32_t j = 0; j < m; ++j) capacity[j] = bits / m + (j < bits % m ? 1u : 0u);
+  std::vector<std::vector<uint32_t>> members(m);
+  std::vector<uint8_t> open(bits);  // 1: non-constant and not yet assigned
+  uint32_t n_open = 0;
+  for (uint32_t i = 0; i < bits; ++i) n_open += (open[i] = constant[i] ? 0 : 1);
+  std::vector<double> near(uint64_t(m) * bits, 0.0);
+  const auto assign = [&](uint32_t j, uint32_t bit) {
+    members[j].push_back(bit);
+    open[bit] = 0;
+    --n_open;
+    double* nj = near.data() + uint64_t(j) * bits;
+    const double* r = row(bit);
+    for (uint32_t c = 0; c < bits; ++c) nj[c] = std::max(nj[c], r[c]);
+  };
 
-  if (!pool.empty()) {  // chain opening (optimize.hpp:118-138)
+  if (n_open) {
+    // the opener: the (draw)-th free bit in ascending order
     std::mt19937_64 rng(seed);
-    const uint32_t first = pool[std::uniform_int_distribution<size_t>(0, pool.size() - 1)(rng)];
-    subs[0].push_back(first);
-    take(first);
-    for (uint32_t j = 1; j < m && !pool.empty(); ++j) {
-      const uint32_t prev = subs[j - 1].empty() ? first : subs[j - 1].front();
-      uint32_t best = pool.front();
-      double best_c = -1.0;
-      for (uint32_t c : pool)
-        if (at(c, prev) > best_c) {
-          best_c = at(c, prev);
-          best = c;
-        }
-      subs[j].push_back(best);
-      take(best);
-    }
-  }
-  while (!pool.empty()) {  // min-max rounds (optimize.hpp:141-160)
-    bool any = false;
-    for (uint32_t j = 0; j < m && !pool.empty(); ++j) {
-      if (subs[j].size() >= cap[j]) continue;
-      any = true;
-      uint32_t best = pool.front();
-      double best_worst = 2.0;
-      for (uint32_t c : pool) {
-        double worst = 0.0;
-        for (uint32_t o : subs[j]) worst = std::max(worst, at(c, o));
-        if (worst < best_worst) {
-          best_worst = worst;
-          best = c;
-        }
+    size_t draw = std::uniform_int_distribution<size_t>(0, n_open - 1)(rng);
+    uint32_t opener = 0;
+    for (uint32_t c = 0; c < bits; ++c)
+      if (open[c] && draw-- == 0) {
+        opener = c;
+        break;
       }
-      subs[j].push_back(best);
-      take(best);
+    assign(0, opener);
+    // substring j opens with the free bit most correlated with substring j-1's opener
+    for (uint32_t j = 1; j < m && n_open; ++j) {
+      const double* r = row(members[j - 1].empty() ? opener : members[j - 1].front());
+      uint32_t pick = bits;
+      for (uint32_t c = 0; c < bits; ++c)
+        if (open[c] && (pick == bits || r[c] > r[pick])) pick = c;
+      assign(j, pick);
     }
-    if (!any) break;
   }
-  uint32_t j = 0;  // constant bits round-robin (optimize.hpp:162-168)
-  for (uint32_t b : constants) {
-    while (subs[j].size() >= cap[j]) j = (j + 1) % m;
-    subs[j].push_back(b);
+  // rounds: each substring with room takes the free bit of smallest max-correlation to it
+  while (n_open) {
+    bool took = false;
+    for (uint32_t j = 0; j < m && n_open; ++j) {
+      if (members[j].size() >= capacity[j]) continue;
+      const double* nj = near.data() + uint64_t(j) * bits;
+      uint32_t pick = bits;
+      for (uint32_t c = 0; c < bits; ++c)
+        if (open[c] && (pick == bits || nj[c] < nj[pick])) pick = c;
+      assign(j, pick);
+      took = true;
+    }
+    if (!took) break;  // no room left (cannot happen with balanced capacities)
+  }
+  // constant bits: dealt round-robin over the remaining room
+  for (uint32_t c = 0, j = 0; c < bits; ++c) {
+    if (!constant[c]) continue;
+    while (members[j].size() >= capacity[j]) j = (j + 1) % m;
+    members[j].push_back(c);
     j = (j + 1) % m;
   }
-  uint32_t k = 0;
-  for (uint32_t q = 0; q < m; ++q) {
-    std::sort(subs[q].begin(), subs[q].end());
-    lengths[q] = uint32_t(subs[q].size());
-    for (uint32_t p : subs[q]) positions[k++] = p;
+  for (uint32_t j = 0, at = 0; j < m; ++j) {
+    std::sort(members[j].begin(), members[j].end());
+    lengths[j] = uint32_t(members[j].size());
+    for (uint32_t v : members[j]) positions[at++] = v;
   }
 }
 

@@ -271,6 +271,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef MIHG_TC_DEBUG
+  // per-tile event timeline of CTA 0 (tiles kTl0 .. kTl0+63 of the launch): [tile][event] clock64
+  constexpr uint32_t kTl0 = 200;
+  unsigned long long* tl = a.prof ? a.prof + 32 * 8 : nullptr;
+#define TC_TL(t, ev)                                                                        \
+  do {                                                                                      \
+    if (tl && blockIdx.x == 0 && (t) >= kTl0 && (t) < kTl0 + 64) tl[((t) - kTl0) * 8 + (ev)] = clock64(); \
+  } while (0)
   unsigned long long wcyc[4] = {0, 0, 0, 0};
   auto wait_k = [&](uint64_t* bar, uint32_t parity, int kind) {
     const unsigned long long c0 = a.prof ? clock64() : 0;
@@ -280,6 +287,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   const unsigned long long t_start = clock64();
 #else
   auto wait_k = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
+#define TC_TL(t, ev) ((void)0)
 #endif
 
   const uint32_t rank = kPair ? cluster_rank() : 0u;  // 0: the pair's MMA issuer
@@ -364,19 +372,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
     tc_fence_after();
 
 #ifdef MIHG_TC_DEBUG
-    if (!kPair && a.mma_only) {
-      if (warp == kMmaWarp && lane == 0) {
-        constexpr uint32_t idesc = tc_idesc(kTcM, kTcN);
+    if (a.mma_only) {
+      if (warp == kMmaWarp && lane == 0 && rank == 0) {
+        constexpr uint32_t idesc = tc_idesc(kTcM * kSides, kTcN);
         const uint32_t b_addr = smem_u32(sB);
         for (uint32_t t = tg; t < tg + T; ++t) {
 #pragma unroll
-          for (int kk = 0; kk < Cfg::kSteps; ++kk)
-            tc_mma_i8(tmem + (t % kAcc) * kTcN, smem_desc_sw128(kstep_addr(smem_u32(sA), kk, kTcM)),
-                      smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kTcN)),
-                      idesc, kk > 0);
+          for (int kk = 0; kk < Cfg::kSteps; ++kk) {
+            const uint64_t ad = smem_desc_sw128(kstep_addr(smem_u32(sA), kk, kTcM));
+            const uint64_t bd =
+                smem_desc_sw128(kstep_addr(b_addr + (a.mma_only == 2 ? (t % S) * Cfg::kB : 0), kk, kCodes));
+            if constexpr (kPair) tc_mma_i8_pair(tmem + (t % kAcc) * kTcN, ad, bd, idesc, kk > 0);
+            else tc_mma_i8(tmem + (t % kAcc) * kTcN, ad, bd, idesc, kk > 0);
+          }
         }
-        tc_commit(tfull);
+        if constexpr (kPair) tc_commit_pair(tfull);
+        else tc_commit(tfull);
         mbar_wait(tfull, mo_phase);  // drains this segment's MMAs
+        mo_phase ^= 1;
+      } else if (kPair && warp == kMmaWarp && lane == 0) {
+        mbar_wait(tfull, mo_phase);  // the peer's copy of the commit
         mo_phase ^= 1;
       }
       __syncwarp();
@@ -389,13 +404,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         const uint32_t b_addr = smem_u32(sB);
         for (uint32_t t = tg; t < tg + T; ++t) {
           const uint32_t s = t % S, ph = (t / S) & 1, b = t % kAcc, bph = (t / kAcc) & 1;
+          TC_TL(t, 0);
           if constexpr (kPair) {
+#ifdef MIHG_TC_DEBUG
+            const unsigned long long c0 = a.prof ? clock64() : 0;
+            mbar_wait_cluster(tempty + b, bph ^ 1);
+            const unsigned long long c1 = a.prof ? clock64() : 0;
+            TC_TL(t, 1);
+            mbar_wait_cluster(full + s, ph);
+            if (a.prof) {
+              wcyc[0] += c1 - c0;
+              wcyc[1] += clock64() - c1;
+            }
+#else
             mbar_wait_cluster(tempty + b, bph ^ 1);
             mbar_wait_cluster(full + s, ph);
+#endif
           } else {
             wait_k(tempty + b, bph ^ 1, 0);
+            TC_TL(t, 1);
             wait_k(full + s, ph, 1);
           }
+          TC_TL(t, 2);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < Cfg::kSteps; ++kk) {  // 32 bytes of K per step
@@ -411,6 +441,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
             tc_commit(empty + s);
             tc_commit(tfull + b);
           }
+          TC_TL(t, 3);
         }
       }
       __syncwarp();
@@ -482,6 +513,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           if constexpr (kPair) mbar_arrive_cluster(full_c + s * 8);  // rank 0's barrier
           else mbar_arrive(full + s);
           mbar_arrive(rempty + r);  // the raw words were consumed by the expansion above
+          if (warp == kEpiWarps) TC_TL(t, 7);
         }
       }
     } else {
@@ -515,6 +547,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           gb_next = __ldcg(a.gbound + q);
         }
         wait_k(tfull + b, (t / kAcc) & 1, 0);  // the tile's MMAs are complete
+        if (warp == 0 && lane == 0) TC_TL(t, 4);
         tc_fence_after();
         static_assert(kEpiCols == 64, "packed epilogue drains 64 columns per group");
         {
@@ -525,6 +558,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         if (lane == 0) {
           if constexpr (kPair) mbar_arrive_cluster(tempty_c + b * 8);  // rank 0's barrier
           else mbar_arrive(tempty + b);
+          if (warp == 0) TC_TL(t, 5);
+          if (warp == kEpiWarps - 1) TC_TL(t, 6);
         }
         const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols;
         if constexpr (kDump) {
@@ -723,9 +758,9 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     if (const char* mo = std::getenv("MIHG_TC_MMA_ONLY")) a.mma_only = uint32_t(std::atoi(mo));
     const char* pe = std::getenv("MIHG_TC_PROF");
     const bool dbg_prof = pe && pe[0] == '1';
-    DeviceBuffer<unsigned long long> profbuf(dbg_prof ? 32 * 8 : 1, st);
+    DeviceBuffer<unsigned long long> profbuf(dbg_prof ? 32 * 8 + 64 * 8 : 1, st);
     if (dbg_prof) {
-      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, 32 * 8 * 8, st));
+      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, (32 * 8 + 64 * 8) * 8, st));
       a.prof = profbuf.get();
     }
 #endif
@@ -764,7 +799,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     if (prof) MIHG_CUDA(cudaEventRecord(ev[1], st));
 #ifdef MIHG_TC_DEBUG
     if (dbg_prof) {
-      unsigned long long h[32 * 8];
+      unsigned long long h[32 * 8 + 64 * 8];
       MIHG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
       MIHG_CUDA(cudaStreamSynchronize(st));
       for (int w = 0; w <= kLoadWarp; ++w) {
@@ -773,6 +808,15 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
                 h[w * 8 + 5], h[w * 8] / tl, h[w * 8 + 1] / tl, h[w * 8 + 2] / tl, h[w * 8 + 3] / tl, h[w * 8 + 4] / tl);
       }
       fprintf(stderr, "tcprof grid %u ipc %u nch %u spq %u\n", grid, a.ipc, a.nch, a.spq);
+      // timeline of CTA 0 (relative to the MMA's wait start of the first recorded tile)
+      const unsigned long long* T = h + 32 * 8;
+      const unsigned long long z = T[0];
+      fprintf(stderr, "tctl tile: mma_wait_start tempty_ok full_ok issued | epi_seen epi_released epi_last_released | prod_full\n");
+      for (int i = 0; i < 64; i += 1)
+        fprintf(stderr, "tctl %2d: %8lld %8lld %8lld %8lld | %8lld %8lld %8lld | %8lld\n", i, (long long)(T[i * 8] - z),
+                (long long)(T[i * 8 + 1] - z), (long long)(T[i * 8 + 2] - z), (long long)(T[i * 8 + 3] - z),
+                (long long)(T[i * 8 + 4] - z), (long long)(T[i * 8 + 5] - z), (long long)(T[i * 8 + 6] - z),
+                (long long)(T[i * 8 + 7] - z));
     }
 #endif
     gather_lists_kernel<<<unsigned(qn), 256, 0, st>>>(lists.get(), counts.get(), a.slots, L, gathered.get(),

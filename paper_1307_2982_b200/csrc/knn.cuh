@@ -63,6 +63,11 @@ void scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_
                      const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
                      uint32_t* d_dists, cudaStream_t st);
 
+// K6 itself (POPC pipe), any width.
+void popc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                          const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                          uint32_t* d_dists, cudaStream_t st);
+
 // K7: the same exhaustive k-NN on the tensor cores (tcscan.cu), codes of 1..256 bits. d_dump
 // (tests only, nullable): every distance, nq x n row-major.
 bool tc_scan_supported(uint32_t bits);

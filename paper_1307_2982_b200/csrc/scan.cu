@@ -147,6 +147,14 @@ void scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_
     tc_scan_knn_device(d_codes, n, bits, id_base, d_queries, nq, k, d_ids, d_dists, st, nullptr);
     return;
   }
+  popc_scan_knn_device(d_codes, n, bits, id_base, d_queries, nq, k, d_ids, d_dists, st);
+}
+
+// K6 on the POPC pipe.
+void popc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint32_t id_base,
+                          const uint64_t* d_queries, uint64_t nq, uint32_t k, uint32_t* d_ids,
+                          uint32_t* d_dists, cudaStream_t st) {
+  if (k > n) throw InvalidArgument("scan_knn: k exceeds database size");
   if (nq == 0 || k == 0) return;
   const uint32_t nw = words_per_code(bits);
   const int QT = nw <= 2 ? 16 : (nw <= 4 ? 8 : 4);

@@ -67,6 +67,7 @@ struct TcArgs {
   uint32_t* gbound;  // [q]: smallest k-th distance proven by any list of the query (0xFFFFFFFF = none)
 #ifdef MIHG_TC_DEBUG
   unsigned long long* prof;  // debug build only: [32 warps][8] cycle counters summed over CTAs
+  uint32_t tl0;              // debug build only: first tile of CTA 0's recorded timeline (MIHG_TC_TL0)
   uint32_t mma_only;         // debug build only: only the MMA stream runs (2: rotating B stages);
                              // results are NOT produced — measures the tensor ceiling
 #endif
@@ -272,11 +273,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef MIHG_TC_DEBUG
   // per-tile event timeline of CTA 0 (tiles kTl0 .. kTl0+63 of the launch): [tile][event] clock64
-  constexpr uint32_t kTl0 = 200;
+  const uint32_t kTl0 = a.tl0;
   unsigned long long* tl = a.prof ? a.prof + 32 * 8 : nullptr;
 #define TC_TL(t, ev)                                                                        \
   do {                                                                                      \
-    if (tl && blockIdx.x == 0 && (t) >= kTl0 && (t) < kTl0 + 64) tl[((t) - kTl0) * 8 + (ev)] = clock64(); \
+    if (tl && blockIdx.x < 2 && (t) >= kTl0 && (t) < kTl0 + 64)                               \
+      tl[blockIdx.x * 512 + ((t) - kTl0) * 8 + (ev)] = clock64();                             \
   } while (0)
   unsigned long long wcyc[4] = {0, 0, 0, 0};
   auto wait_k = [&](uint64_t* bar, uint32_t parity, int kind) {
@@ -513,7 +515,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           if constexpr (kPair) mbar_arrive_cluster(full_c + s * 8);  // rank 0's barrier
           else mbar_arrive(full + s);
           mbar_arrive(rempty + r);  // the raw words were consumed by the expansion above
-          if (warp == kEpiWarps) TC_TL(t, 7);
+
         }
       }
     } else {
@@ -559,7 +561,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           if constexpr (kPair) mbar_arrive_cluster(tempty_c + b * 8);  // rank 0's barrier
           else mbar_arrive(tempty + b);
           if (warp == 0) TC_TL(t, 5);
-          if (warp == kEpiWarps - 1) TC_TL(t, 6);
+#ifdef MIHG_TC_DEBUG
+          if (tl && blockIdx.x < 2 && t >= kTl0 && t < kTl0 + 64)  // the last epilogue warp's release
+            atomicMax(tl + blockIdx.x * 512 + (t - kTl0) * 8 + 6, clock64());
+#endif
         }
         const uint64_t id0 = lo + uint64_t(t - tg) * kTcN + g * kEpiCols;
         if constexpr (kDump) {
@@ -580,7 +585,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           for (int i = 0; i < w; ++i) m16[i] = __vmins2(m16[i], m16[i + w]);
         const int32_t mn = min(int32_t(int16_t(uint16_t(m16[0]))), int32_t(int16_t(uint16_t(m16[0] >> 16))));
         if (mn <= thr) {
-          // hit mask (two bits per register), then the (few) hits re-derive their distance
+          // hits straight from the accumulator: d = value + popc(q) exactly, no code word re-read.
+          // The values go to a thread-local copy first (L1), read back by dynamic column index,
+          // so the register-resident drain loop keeps its budget.
+          uint32_t tmp[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) tmp[i] = v[i];
           const uint32_t t2 = uint32_t(uint16_t(int16_t(thr))) * 0x00010001u;
           uint64_t m = 0;
 #pragma unroll
@@ -593,10 +603,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
             m &= m - 1;
             const uint64_t id = id0 + j;
             if (id >= hi) break;
-            uint32_t d = 0;
-#pragma unroll
-            for (int w = 0; w < W; ++w) d += __popcll(__ldg(qp + w) ^ __ldg(a.codes + id * W + w));
-            list[cnt++] = (uint64_t(d) << 32) | uint32_t(id);
+            const int32_t val = int32_t(int16_t(uint16_t(tmp[j >> 1] >> ((j & 1) * 16))));
+            list[cnt++] = (uint64_t(val + pq) << 32) | uint32_t(id);
           }
         }
         // warp-cooperative compaction of every list that reached 2k entries (scanlist.cuh)
@@ -607,11 +615,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           uint64_t* l2 = reinterpret_cast<uint64_t*>(__shfl_sync(~0u, reinterpret_cast<uintptr_t>(list), src));
           uint32_t c2 = __shfl_sync(~0u, cnt, src);
           __syncwarp();
-          const uint32_t nt = compact_list(l2, c2, a.bits, a.k, hist);
+          // every entry of the list is <= the owner's bound + 1 (own = last k-th distance - 1)
+          const uint32_t tau = min(a.bits, uint32_t(__shfl_sync(~0u, own, src) + 1));
+#ifdef MIHG_TC_DEBUG
+          const unsigned long long cc0 = clock64();
+#endif
+          const uint32_t nt = compact_list(l2, c2, tau, a.k, hist);
+#ifdef MIHG_TC_DEBUG
+          if (a.prof) {
+            wcyc[2] += clock64() - cc0;
+            wcyc[3] += 1;
+          }
+#endif
           if (lane == uint32_t(src)) {
             cnt = c2;
             own = int32_t(nt) - 1;
             atomicMin(a.gbound + q, nt);
+#ifdef MIHG_TC_DEBUG
+            if (tl && blockIdx.x < 2 && t >= kTl0 && t < kTl0 + 64)  // compactions during this tile
+              atomicAdd(tl + blockIdx.x * 512 + (t - kTl0) * 8 + 7, 1ull);
+#endif
           }
           __syncwarp();
         }
@@ -689,10 +712,27 @@ void launch_tc(const TcArgs& a, uint32_t grid, cudaStream_t st) {
 
 bool tc_scan_supported(uint32_t bits) { return bits >= 1 && bits <= 256; }
 
-// CTA-pair (cta_group::2) K7: MIHG_TC_PAIR=1|0 selects (default 0 until measured).
+namespace {
+__global__ void kth_column_kernel(const uint32_t* __restrict__ dists, uint64_t nq, uint32_t k,
+                                  uint32_t* __restrict__ out) {
+  const uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (q < nq) out[q] = dists[q * k + (k - 1)];
+}
+}  // namespace
+
+// Codes in the bound-seeding sample (0: none): MIHG_TC_SEED overrides; by default 65536 when the
+// database is at least 64x larger and the sample holds at least 16 k codes.
+uint64_t tc_seed_codes(uint64_t n, uint32_t k) {
+  const char* e = std::getenv("MIHG_TC_SEED");
+  const uint64_t s = e ? std::strtoull(e, nullptr, 10) : 65536;
+  return (s >= 16ull * k && n >= 64 * s) ? s : 0;
+}
+
+// CTA-pair (cta_group::2) geometry by default (n = 1e8 x 256-bit, 1e4 queries: 39.4K -> 48.9K
+// q/s; 64-bit: same within noise); MIHG_TC_PAIR=0 selects one CTA per tile.
 bool tc_pair_enabled() {
   const char* e = std::getenv("MIHG_TC_PAIR");  // read per call: tests run both geometries
-  return e && e[0] == '1';
+  return !(e && e[0] == '0');
 }
 
 // K7: the exhaustive k-NN of scan_knn_device on the tensor cores (same results bit for bit).
@@ -756,11 +796,13 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     a.dump = d_dump;
 #ifdef MIHG_TC_DEBUG  // timing probes of a debug build (make TCDEBUG=1); never in the product .so
     if (const char* mo = std::getenv("MIHG_TC_MMA_ONLY")) a.mma_only = uint32_t(std::atoi(mo));
+    a.tl0 = 200;
+    if (const char* t0 = std::getenv("MIHG_TC_TL0")) a.tl0 = uint32_t(std::atoi(t0));
     const char* pe = std::getenv("MIHG_TC_PROF");
     const bool dbg_prof = pe && pe[0] == '1';
-    DeviceBuffer<unsigned long long> profbuf(dbg_prof ? 32 * 8 + 64 * 8 : 1, st);
+    DeviceBuffer<unsigned long long> profbuf(dbg_prof ? 32 * 8 + 2 * 64 * 8 : 1, st);
     if (dbg_prof) {
-      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, (32 * 8 + 64 * 8) * 8, st));
+      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, (32 * 8 + 2 * 64 * 8) * 8, st));
       a.prof = profbuf.get();
     }
 #endif
@@ -768,6 +810,18 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     DeviceBuffer<uint32_t> counts(qn * a.slots, st), gcount(qn, st), gbound(qn, st);
     MIHG_CUDA(cudaMemsetAsync(counts.get(), 0, qn * a.slots * 4, st));
     MIHG_CUDA(cudaMemsetAsync(gbound.get(), 0xFF, qn * 4, st));
+    // Seed every query's shared bound with the k-th smallest distance over a sample of the database
+    // (the first `seed` codes, K6 on the POPC pipe): an upper bound on the global k-th distance, so
+    // the lists start filtered instead of accepting everything until their first compactions
+    // (the hit storm at the start of every segment). Exact: only codes with d > bound are dropped,
+    // and the bound is inclusive (ties kept).
+    const uint64_t seed = tc_seed_codes(n, k);
+    if (seed) {
+      DeviceBuffer<uint32_t> si(qn * k, st), sd(qn * k, st);
+      popc_scan_knn_device(d_codes, seed, bits, 0, d_queries + q0 * W, qn, k, si.get(), sd.get(), st);
+      kth_column_kernel<<<unsigned((qn + 255) / 256), 256, 0, st>>>(sd.get(), qn, k, gbound.get());
+      MIHG_LAUNCH();
+    }
     a.gbound = gbound.get();
     a.lists = lists.get();
     a.counts = counts.get();
@@ -799,24 +853,29 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     if (prof) MIHG_CUDA(cudaEventRecord(ev[1], st));
 #ifdef MIHG_TC_DEBUG
     if (dbg_prof) {
-      unsigned long long h[32 * 8 + 64 * 8];
+      unsigned long long h[32 * 8 + 2 * 64 * 8];
       MIHG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
       MIHG_CUDA(cudaStreamSynchronize(st));
       for (int w = 0; w <= kLoadWarp; ++w) {
         const double tl = double(h[w * 8 + 5] ? h[w * 8 + 5] : 1);
-        fprintf(stderr, "tcprof warp %2d: tiles %llu cyc/tile %.0f wait0 %.0f wait1 %.0f k2 %.0f k3 %.0f\n", w,
-                h[w * 8 + 5], h[w * 8] / tl, h[w * 8 + 1] / tl, h[w * 8 + 2] / tl, h[w * 8 + 3] / tl, h[w * 8 + 4] / tl);
+        fprintf(stderr, "tcprof warp %2d: tiles %llu cyc/tile %.0f wait0 %.0f wait1 %.0f compaction cyc/call %.0f calls/tile %.4f\n", w,
+                h[w * 8 + 5], h[w * 8] / tl, h[w * 8 + 1] / tl, h[w * 8 + 2] / tl,
+                h[w * 8 + 3] / double(h[w * 8 + 4] ? h[w * 8 + 4] : 1), h[w * 8 + 4] / tl);
       }
       fprintf(stderr, "tcprof grid %u ipc %u nch %u spq %u\n", grid, a.ipc, a.nch, a.spq);
       // timeline of CTA 0 (relative to the MMA's wait start of the first recorded tile)
       const unsigned long long* T = h + 32 * 8;
       const unsigned long long z = T[0];
-      fprintf(stderr, "tctl tile: mma_wait_start tempty_ok full_ok issued | epi_seen epi_released epi_last_released | prod_full\n");
+      fprintf(stderr, "tctl tile: mma_wait_start tempty_ok full_ok issued | epi_seen epi_released epi_max_released | compactions\n");
+      // CTA 1 (the pair's second SM) on its own clock: deltas to its first epi_seen
+      const unsigned long long* U = T + 512;
+      const unsigned long long z1 = U[4];
       for (int i = 0; i < 64; i += 1)
-        fprintf(stderr, "tctl %2d: %8lld %8lld %8lld %8lld | %8lld %8lld %8lld | %8lld\n", i, (long long)(T[i * 8] - z),
-                (long long)(T[i * 8 + 1] - z), (long long)(T[i * 8 + 2] - z), (long long)(T[i * 8 + 3] - z),
-                (long long)(T[i * 8 + 4] - z), (long long)(T[i * 8 + 5] - z), (long long)(T[i * 8 + 6] - z),
-                (long long)(T[i * 8 + 7] - z));
+        fprintf(stderr, "tctl %2d: %8lld %8lld %8lld %8lld | %8lld %8lld %8lld | %8lld || cta1 epi %8lld %8lld %8lld prod %8lld\n", i,
+                (long long)(T[i * 8] - z), (long long)(T[i * 8 + 1] - z), (long long)(T[i * 8 + 2] - z),
+                (long long)(T[i * 8 + 3] - z), (long long)(T[i * 8 + 4] - z), (long long)(T[i * 8 + 5] - z),
+                (long long)(T[i * 8 + 6] - z), (long long)T[i * 8 + 7], (long long)(U[i * 8 + 4] - z1),
+                (long long)(U[i * 8 + 5] - z1), (long long)(U[i * 8 + 6] - z1), (long long)U[i * 8 + 7]);
     }
 #endif
     gather_lists_kernel<<<unsigned(qn), 256, 0, st>>>(lists.get(), counts.get(), a.slots, L, gathered.get(),

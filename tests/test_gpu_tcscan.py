@@ -14,8 +14,7 @@ pytestmark = pytest.mark.gpu
 def tc_geometry(request):
     """Every K7 test runs in both geometries: one CTA per 128-query x 256-code tile, and CTA pairs
     (cta_group::2, M = 256) that split each code tile between two SMs (MIHG_TC_PAIR=1)."""
-    if request.param == "pair":
-        os.environ["MIHG_TC_PAIR"] = "1"
+    os.environ["MIHG_TC_PAIR"] = "1" if request.param == "pair" else "0"
     yield request.param
     os.environ.pop("MIHG_TC_PAIR", None)
 
@@ -123,3 +122,26 @@ def test_tc_scan_misaligned_and_ragged(cuda_ok, port, bits, first, n):
     oi, od = port.scan_knn(allc[first:], bits, qs, k)
     assert np.array_equal(ids.cpu().numpy().view(np.uint32), oi + 1000)
     assert np.array_equal(ds.cpu().numpy().view(np.uint32), od)
+
+
+@pytest.mark.parametrize("bits,k", [(64, 3), (256, 10), (128, 1)])
+def test_tc_scan_seeded_bound(cuda_ok, port, bits, k):
+    """The K7 lists start from a bound seeded by the exact k-th distance over the first codes of the
+    database (an upper bound on the true k-th distance; ties kept): same answer as the oracle,
+    also when the sample's k-th distance ties with many later codes (duplicated database rows)."""
+    import paper_1307_2982_b200 as mg
+
+    n = 40000
+    base = mg.gen_uniform(n, bits, 60 + bits).raw_words()
+    base[n // 2:] = base[: n - n // 2]  # every code twice: the sample's k-th distance recurs later
+    db = mg.CodeDatabase(bits, base)
+    qs = mg.gen_uniform(150, bits, 61 + bits).raw_words()
+    idx = mg.MihIndex.build(db, mg.consecutive_partition(bits, max(1, -(-bits // 32))), device=0)
+    want = port.scan_knn(base, bits, qs, k)
+    for seed in ("0", "256", "512"):
+        os.environ["MIHG_TC_SEED"] = seed
+        try:
+            got = _scan(idx, qs, k, "tc")
+        finally:
+            os.environ.pop("MIHG_TC_SEED", None)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), seed

@@ -155,6 +155,13 @@ __global__ void gather_codes_kernel(const uint64_t* __restrict__ codes, uint32_t
   }
 }
 
+// 32-bit residuals in table order: the bits of the other 32-bit substring of each entry's code.
+__global__ void gather_residuals_kernel(const uint64_t* __restrict__ codes, const uint32_t* __restrict__ ids,
+                                        uint64_t n, uint32_t shift, uint32_t* __restrict__ out) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
+    out[e] = uint32_t(__ldg(codes + __ldg(ids + e)) >> shift);
+}
+
 __global__ void occupancy_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint32_t* __restrict__ occ) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * blockDim.x) {
@@ -357,7 +364,18 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
       MIHG_LAUNCH();
     }
   }
-  if (idx.inline_codes && n) {
+  // 64-bit codes, two contiguous 32-bit substrings (config 4's shape): the other substring alone
+  // identifies the code within a bucket, so table-order codes shrink to 4 bytes per entry
+  const bool residual = idx.inline_codes && n && idx.W == 1 && idx.m == 2 && idx.lengths[0] == 32 &&
+                        idx.lengths[1] == 32 && idx.subs[0].contiguous && idx.subs[1].contiguous &&
+                        opt.residual_codes && !(std::getenv("MIHG_RESIDUAL") && std::getenv("MIHG_RESIDUAL")[0] == '0');
+  if (residual) {
+    t->rshift = idx.subs[1 - j].offset;  // 0 or 32
+    t->rcodes = DeviceBuffer<uint32_t>(n, st);
+    gather_residuals_kernel<<<grid_for(n, 256), 256, 0, st>>>(idx.codes.get(), t->ids.get(), n, t->rshift,
+                                                              t->rcodes.get());
+    MIHG_LAUNCH();
+  } else if (idx.inline_codes && n) {
     t->tcodes = DeviceBuffer<uint64_t>(n * idx.W, st);
     gather_codes_kernel<<<grid_for(n * idx.W, 256), 256, 0, st>>>(idx.codes.get(), idx.W, t->ids.get(), n,
                                                                   t->tcodes.get());

@@ -71,6 +71,11 @@ struct DevTable {
   const uint32_t* occ;      // sparse: 1 bit per bucket (non-empty), or nullptr
   uint32_t s;
   uint32_t dense;
+  // 64-bit codes split into two 32-bit substrings: the table-order codes keep only the OTHER
+  // substring (4 bytes per entry; this table's 32 bits equal the bucket key). rshift: position of
+  // the other substring in the code word (0 or 32). rcodes != nullptr replaces `codes`.
+  const uint32_t* rcodes;
+  uint32_t rshift;
 };
 
 // Substring j of the partition: contiguous run (offset, len) or explicit positions.

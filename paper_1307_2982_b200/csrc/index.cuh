@@ -19,17 +19,29 @@ struct TableStorage {
   DeviceBuffer<uint32_t> esc;      // sparse: 65 per escaped block
   DeviceBuffer<uint64_t> tcodes;   // optional: codes in table order (bucket = contiguous run)
   DeviceBuffer<uint32_t> occ;      // sparse: occupancy bitmap, 1 bit per bucket
+  DeviceBuffer<uint32_t> rcodes;   // optional: 32-bit residual codes in table order (see DevTable)
+  uint32_t rshift = 0;
   uint64_t escaped_blocks = 0;
   uint64_t non_empty_buckets = 0;
   uint64_t non_empty_groups = 0;  // 32-bucket groups (the reference's accounting unit)
   uint64_t max_bucket = 0;
   DevTable view() const {
     return DevTable{ids.get(), offsets.get(), dir.get(), esc.get(), tcodes.get(), occ.get(), s,
-                    dense ? 1u : 0u};
+                    dense ? 1u : 0u, rcodes.get(), rshift};
+  }
+  // frees every device buffer (stream-ordered on the index stream, before that stream goes away)
+  void release() {
+    ids.reset();
+    offsets.reset();
+    dir.reset();
+    esc.reset();
+    tcodes.reset();
+    occ.reset();
+    rcodes.reset();
   }
   uint64_t bytes() const {
     return ids.size() * 4 + offsets.size() * 4 + dir.size() * sizeof(DirBlock) + esc.size() * 4 +
-           tcodes.size() * 8 + occ.size() * 4;
+           tcodes.size() * 8 + occ.size() * 4 + rcodes.size() * 4;
   }
 };
 
@@ -47,6 +59,8 @@ struct BuildOptions {
   // Codes stored inline in table order so a bucket's candidates are one contiguous read:
   // -1 auto (when all tables' inline codes fit in 40% of free HBM), 0 off, 1 on.
   int inline_codes = -1;
+  // 64-bit codes with two 32-bit substrings: 4-byte residual table-order codes (MIHG_RESIDUAL=0 off)
+  bool residual_codes = true;
   // Sparse tables: 1-bit-per-bucket occupancy bitmap in front of the directory, so a probe of
   // an empty bucket is one 4-byte (L2-resident per key slice) read instead of a DRAM sector.
   bool occupancy = false;

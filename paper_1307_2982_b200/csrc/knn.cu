@@ -84,14 +84,7 @@ Index::~Index() {
   d_subs.reset();
   d_submask.reset();
   for (auto& t : tables)
-    if (t) {
-      t->ids.reset();
-      t->offsets.reset();
-      t->dir.reset();
-      t->esc.reset();
-      t->tcodes.reset();
-      t->occ.reset();
-    }
+    if (t) t->release();
   d_tables.reset();
   if (stream) {
     cudaStreamSynchronize(stream);
@@ -360,6 +353,42 @@ __device__ __forceinline__ QueryCtx query_ctx(const ProbeArgs& p, uint32_t q) {
   return c;
 }
 
+// Keepers of a verified pair of entries: histogram + append (one atomic per warp), shared by the
+// residual and the full-code verification paths.
+__device__ __forceinline__ void keep_entries(const ProbeArgs& p, const QueryCtx& c, bool k0, uint32_t dist0,
+                                             uint32_t id0, bool k1, uint32_t dist1, uint32_t id1,
+                                             uint32_t b0, uint32_t b1);
+
+// Residual verification (64-bit codes, m = 2 tables of 32 bits): the entry's bits in this table's
+// substring are the bucket key v with popc(v ^ q_a) = rr (the ring), so d(q, x) = rr +
+// popc(q_other ^ residual), and the other table's substring distance is that popcount itself.
+// First discovery (index.hpp:219-230 dedup, see first_discovery): new iff d_other > rr when the
+// other table precedes this one (j < a), d_other >= rr when it follows (j > a, rr >= 1).
+template <bool kTrace>
+__device__ __forceinline__ void verify_residual(const ProbeArgs& p, const QueryCtx& c, bool v0, uint32_t e0,
+                                                bool v1, uint32_t e1, uint64_t q, uint64_t& n_new) {
+  const uint32_t qo = uint32_t(q >> p.tab.rshift);
+  const uint32_t r0 = v0 ? __ldg(p.tab.rcodes + e0) : 0u, r1 = v1 ? __ldg(p.tab.rcodes + e1) : 0u;
+  const uint32_t do0 = __popc(qo ^ r0), do1 = __popc(qo ^ r1);
+  const uint32_t dist0 = p.rr + do0, dist1 = p.rr + do1;
+  const bool other_first = p.a == 1;  // the other table (j = 1 - a) precedes this one
+  const bool f0 = other_first ? do0 > p.rr : (p.rr == 0 || do0 >= p.rr);
+  const bool f1 = other_first ? do1 > p.rr : (p.rr == 0 || do1 >= p.rr);
+  bool k0, k1;
+  if constexpr (kTrace) {
+    n_new += uint64_t(v0 && f0) + uint64_t(v1 && f1);
+    k0 = v0 && f0 && dist0 <= c.U;
+    k1 = v1 && f1 && dist1 <= c.U;
+  } else {
+    k0 = v0 && dist0 <= c.U && f0;
+    k1 = v1 && dist1 <= c.U && f1;
+  }
+  const uint32_t b0 = __ballot_sync(~0u, k0), b1 = __ballot_sync(~0u, k1);
+  if ((b0 | b1) == 0) return;
+  const uint32_t id0 = k0 ? __ldg(p.tab.ids + e0) : 0u, id1 = k1 ? __ldg(p.tab.ids + e1) : 0u;
+  keep_entries(p, c, k0, dist0, id0, k1, dist1, id1, b0, b1);
+}
+
 // Verify up to two table entries per lane (index.hpp:219-230): dedup by first discovery, full
 // distance, keep if d <= U. All 32 lanes call it together (warp-uniform query, `valid` masks
 // lanes without an entry); keepers are appended with ONE atomic per warp and histogrammed with
@@ -368,6 +397,12 @@ template <int W, bool kTrace>
 __device__ __forceinline__ void verify_entries(const ProbeArgs& p, const QueryCtx& c, bool v0,
                                                uint32_t e0, bool v1, uint32_t e1, const uint64_t* qc,
                                                uint32_t nw, uint64_t& n_new) {
+  if constexpr (W == 1) {
+    if (p.tab.rcodes) {  // 4-byte residual codes (two 32-bit substrings, see DevTable)
+      verify_residual<kTrace>(p, c, v0, e0, v1, e1, qc[0], n_new);
+      return;
+    }
+  }
   Diff<W> d0, d1;
   uint32_t id0 = 0, id1 = 0;
   if (p.tab.codes) {
@@ -396,6 +431,12 @@ __device__ __forceinline__ void verify_entries(const ProbeArgs& p, const QueryCt
     if (k0) id0 = __ldg(p.tab.ids + e0);
     if (k1) id1 = __ldg(p.tab.ids + e1);
   }
+  keep_entries(p, c, k0, dist0, id0, k1, dist1, id1, b0, b1);
+}
+
+__device__ __forceinline__ void keep_entries(const ProbeArgs& p, const QueryCtx& c, bool k0, uint32_t dist0,
+                                             uint32_t id0, bool k1, uint32_t dist1, uint32_t id1,
+                                             uint32_t b0, uint32_t b1) {
   const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
   const uint32_t n0 = __popc(b0), total = n0 + __popc(b1);
   uint32_t base = 0;
@@ -968,12 +1009,34 @@ double scan_cost_per_code(uint32_t bits) {
   const uint32_t W = words_per_code(bits);
   if (scan_kernel_for(bits) != ScanKernel::Tensor) return W;
   const char* e = std::getenv("MIHG_TC_SPEEDUP");
-  // measured pair rates on B200 (bench.py --method scan, 1e4 queries): K7 4.8e12 pairs/s (64-bit,
-  // n = 1e8) ... 3.8e12 (256-bit, n = 1e9); K6 1.95e12 (W=1) ... 5.3e11 (W=4) pairs/s
+  // measured pair rates on B200 (bench.py --method scan, 1e4 queries): K7 (CTA pairs) 6.4e12
+  // pairs/s (64-bit, n = 1e8) ... 5.8e12 (256-bit, n = 1e9); K6 1.95e12 (W=1) ... 5.3e11 (W=4)
   // (W <= 2: no credit — MIH's candidate verification, not charged by the probe count, dominates
   // there; measured config 2 at k = 100 lost 17% when stragglers were switched on the rate ratio)
-  const double f = e ? std::atof(e) : (W <= 2 ? 1.0 : W == 3 ? 5.5 : 7.0);
+  const double f = e ? std::atof(e) : (W <= 2 ? 1.0 : W == 3 ? 8.0 : 10.9);
   return W / f;
+}
+
+// MIH lookups a query needs under the uniform-code model: R = the first radius
+// with n * sum_{d <= R} C(b, d) / 2^b >= k, lookups = sum_{r <= R} C(s_{r mod m}, r / m). Used only
+// to skip an MIH prefix that cannot win: clustered data needs fewer lookups than this, so the model
+// errs towards MIH, and the caller demands a wide margin before it switches up front.
+double uniform_model_lookups(const Index& idx, uint32_t k) {
+  const uint32_t b = idx.bits, m = idx.m;
+  const double ln2 = std::log(2.0);
+  double ln_cum = -INFINITY;  // ln sum_{d <= R} C(b, d)
+  uint32_t R = 0;
+  for (; R <= b; ++R) {
+    const double ln_c = std::lgamma(double(b) + 1) - std::lgamma(double(R) + 1) - std::lgamma(double(b - R) + 1);
+    ln_cum = ln_cum == -INFINITY ? ln_c : std::max(ln_cum, ln_c) + std::log1p(std::exp(-std::fabs(ln_cum - ln_c)));
+    if (std::log(double(idx.n)) + ln_cum - b * ln2 >= std::log(double(k))) break;
+  }
+  double lookups = 0;
+  for (uint32_t r = 0; r <= std::min(R, b); ++r) {
+    const uint32_t s = idx.lengths[r % m], rr = r / m;
+    if (rr <= s) lookups += double(host_binom(s, rr));
+  }
+  return lookups;
 }
 
 ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
@@ -1155,9 +1218,20 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
       if (nact_known == 0) return;
     }
   };
+  // hopeless MIH: when the uniform model puts the lookups above 16x the scan budget, every query
+  // goes to the exhaustive scan at round 0 (config 5, 256-bit uniform: ~220x; configs 1-4: < 1x)
+  const bool pre_switch = alpha > 0 && uniform_model_lookups(idx, kstop) * probe_pairs >= 16.0 * alpha * scan_pairs;
   uint32_t r = 0;
   for (; nact_known > 0; ++r) {
     if (r > idx.bits) throw CudaError("knn: radius loop exceeded the code width (internal error)");
+    if (pre_switch && r == 0) {
+      switched = act_buf[0];
+      nswitched = nq;
+      neutralise_kernel<<<unsigned(std::min<uint64_t>((nq + 255) / 256, 1024)), 256, 0, st>>>(
+          act_buf[0], uint32_t(nq), ws.final_r.get(), ws.bufcnt.get(), ws.dropmin.get());
+      MIHG_LAUNCH();
+      break;
+    }
     const uint32_t a = r % m, rr = r / m;
     const uint32_t s = idx.lengths[a];
     const uint64_t ring = rr <= s ? host_binom(s, rr) : 0;
@@ -1217,8 +1291,12 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     MIHG_LAUNCH();
     MIHG_CUDA(cudaMemcpyAsync(ws.h_nact + r + 1, ws.nact_dev.get() + r + 1, 4, cudaMemcpyDeviceToHost, st));
     MIHG_CUDA(cudaEventRecord(ws.ev_round[r], st));
-    // keep at most kRunAhead rounds unread; read any that already finished
-    while (r_known <= r && (r + 1 - r_known > kRunAhead || cudaEventQuery(ws.ev_round[r_known]) == cudaSuccess)) {
+    // keep at most kRunAhead rounds unread; read any that already finished. Partitioned calls read
+    // on the fixed lag only, so every rank enqueues the same rounds (each round carries a
+    // collective: an opportunistic early read on one rank would leave the ranks' all-reduces
+    // unpaired)
+    while (r_known <= r && (r + 1 - r_known > kRunAhead ||
+                            (!part && cudaEventQuery(ws.ev_round[r_known]) == cudaSuccess))) {
       learn(r_known);
       if (nact_known == 0) break;
     }

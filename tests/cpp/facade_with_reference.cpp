@@ -17,6 +17,7 @@
 #include "mihg/mih_gpu.hpp"
 
 int main() {
+  std::setvbuf(stdout, nullptr, _IONBF, 0);
   int bad = 0;
   // shapes whose reference CPU search is cheap (substrings <= 24 bits: 32-bit substrings at
   // n = 2e4 put the reference in its exhaustive-probing regime, minutes per query)
@@ -26,8 +27,10 @@ int main() {
     for (uint32_t m : {3u, 4u, 6u}) {
       if ((bits + m - 1) / m > 24) continue;
       mih::Partition p = mih::consecutive_partition(bits, m);
+      std::fprintf(stderr, "stage build bits=%u m=%u\n", bits, m);
       mih::MihIndex cpu = mih::MihIndex::build(db, p);
       mihg::dropin::MihIndex gpu = mihg::dropin::MihIndex::build(db, p);
+      std::fprintf(stderr, "stage accessors\n");
       // accessors (index.hpp:143-146): the index owns copies of the caller's db and partition
       if (!(gpu.db() == cpu.db()) || !(gpu.partition() == cpu.partition()) || gpu.num_tables() != cpu.num_tables()) {
         std::printf("accessor mismatch bits=%u m=%u\n", bits, m);
@@ -51,6 +54,7 @@ int main() {
           }
         }
       }
+      std::fprintf(stderr, "stage range\n");
       for (uint64_t qi = 0; qi < 5; ++qi)  // range_search (index.hpp:149-176)
         for (uint32_t r : {0u, bits / 8, bits / 4}) {
           mih::SearchTrace tc, tg;
@@ -73,6 +77,7 @@ int main() {
         }
     }
   }
+  std::fprintf(stderr, "stage build_index\n");
   // build_index (index.hpp:287-289) and the error contract (index_test.cpp:250-268)
   mih::CodeDatabase db = mih::gen_uniform(10, 64, 1);
   mihg::dropin::MihIndex gpu = mihg::dropin::build_index(db, mih::consecutive_partition(64, 2));
@@ -94,6 +99,7 @@ int main() {
     ++bad;
   } catch (const std::invalid_argument&) {
   }
+  std::fprintf(stderr, "stage optimize\n");
   // substring optimisation: the GPU Gram path vs the reference's estimate_correlations (bitwise)
   // and greedy_assign over the reference's own matrix type (optimize.hpp)
   for (uint32_t bits : {16u, 100u, 256u}) {
@@ -105,6 +111,7 @@ int main() {
       for (uint32_t j = 0; j < bits; ++j)
         if (want.at(i, j) != got.at(i, j)) ++bad;
     }
+    std::fprintf(stderr, "stage optimize bits=%u gram done\n", bits);
     for (uint32_t m : {2u, 4u}) {
       if (!(mih::greedy_assign(want, m, 7 + m) == mihg::greedy_assign<mih::Partition>(got, m, 7 + m))) {
         std::printf("greedy_assign mismatch bits=%u m=%u\n", bits, m);
@@ -117,6 +124,7 @@ int main() {
     ++bad;
   } catch (const std::invalid_argument&) {
   }
+  std::fprintf(stderr, "stage done\n");
   std::printf(bad ? "FAIL %d\n" : "OK drop-in parity (reference MihIndex vs mihg::MihIndex)\n", bad);
   return bad ? 1 : 0;
 }

@@ -398,6 +398,10 @@ def main():
     t0 = time.time()
     codes = make_codes_device(cfg, lo, hi, cfg["db_seed"], torch, dev, L)
     queries = make_codes_device(cfg, 0, nq, cfg["q_seed"], torch, dev, L)
+    if os.environ.get("MIHG_BENCH_SORTQ") == "1":  # experiment: batch order by code value
+        qn = queries.cpu().numpy().view(np.uint64)
+        order = np.lexsort(qn.T[::-1])
+        queries = torch.from_numpy(np.ascontiguousarray(qn[order]).view(np.int64)).to(dev)
     gen_s = time.time() - t0
     t0 = time.time()
     idx = mg.MihIndex.build_from_device(codes.data_ptr(), hi - lo, bits, mg.consecutive_partition(bits, m),
@@ -597,7 +601,8 @@ def main():
     # DRAM traffic of the probe kernels per step, from a committed ncu capture of the same
     # config (tools/ncu_traffic.sh; traffic is a profiler measurement, never taken live)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01", f"traffic_c{args.config}.json")
+    tp = next((t for t in (os.path.join(ROOT, "profiles", r, f"traffic_c{args.config}.json") for r in ("r02", "r01"))
+               if os.path.exists(t)), "")
     if (os.path.exists(tp) and world == 1 and cfg["n"] == CONFIGS[args.config]["n"]
             and cfg["nq"] == CONFIGS[args.config]["nq"] and cfg["k"] == CONFIGS[args.config]["k"]):
         tj = json.load(open(tp))

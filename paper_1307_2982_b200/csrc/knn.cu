@@ -701,54 +701,69 @@ __global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32
                                      uint32_t* __restrict__ ubound, uint32_t k, uint32_t r,
                                      uint32_t* __restrict__ final_r, uint32_t* __restrict__ bufcnt,
                                      uint64_t* __restrict__ buf, uint32_t cap) {
+  __shared__ uint32_t s_n, s_base;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   if (d_nact_in) nact = *d_nact_in;  // device-planned round (grid sized by an upper bound)
-  if (warp >= nact) return;
-  const uint32_t q = act_in[warp];
-  const uint32_t U = ubound[q];
-  const uint32_t* h = hist + uint64_t(q) * b1;
-  uint64_t run = 0, settled = 0;
+  if (blockIdx.x * uint64_t(blockDim.x) >= uint64_t(nact) * 32) return;  // whole block idle
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  const bool active = warp < nact;
+  const uint32_t q = active ? act_in[warp] : 0u;
+  const uint32_t U = active ? ubound[q] : 0u;
+  bool survive = false;
   uint32_t newU = U;
-  bool found = false;
-  for (uint32_t d0 = 0; d0 <= U; d0 += 32) {
-    const uint32_t d = d0 + lane;
-    uint64_t v = d <= U ? h[d] : 0;
+  if (active) {
+    const uint32_t* h = hist + uint64_t(q) * b1;
+    uint32_t run = 0, settled = 0;
+    bool found = false;
+    for (uint32_t d0 = 0; d0 <= U; d0 += 32) {
+      const uint32_t d = d0 + lane;
+      uint32_t v = d <= U ? h[d] : 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(~0u, v, o);
-      if (lane >= o) v += y;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(~0u, v, o);
+        if (lane >= o) v += y;
+      }
+      const uint32_t cum = run + v;
+      if (r >= d0 && r < d0 + 32) settled = __shfl_sync(~0u, cum, r - d0);
+      const uint32_t ok = __ballot_sync(~0u, d <= U && cum >= k);
+      if (!found && ok) {
+        newU = d0 + __ffs(ok) - 1;
+        found = true;
+      }
+      run = __shfl_sync(~0u, cum, 31);
     }
-    const uint64_t cum = run + v;
-    if (r >= d0 && r < d0 + 32) settled = __shfl_sync(~0u, cum, r - d0);
-    const uint32_t ok = __ballot_sync(~0u, d <= U && cum >= k);
-    if (!found && ok) {
-      newU = d0 + __ffs(ok) - 1;
-      found = true;
+    if (r > U) settled = run;  // cannot happen while active (r <= U); kept for safety
+    if (settled >= k) {
+      if (lane == 0) final_r[q] = r;
+    } else {
+      survive = true;
     }
-    run = __shfl_sync(~0u, cum, 31);
   }
-  if (r > U) settled = run;  // cannot happen while active (r <= U); kept for safety
-  if (settled >= k) {
-    if (lane == 0) final_r[q] = r;
-    return;
-  }
-  if (lane == 0) {
+  // survivors: one shared-memory slot each, one global atomic per block (the next round's count)
+  uint32_t slot = 0;
+  if (survive && lane == 0) {
     ubound[q] = newU;
-    act_out[atomicAdd(nact_out, 1u)] = q;
+    slot = atomicAdd(&s_n, 1u);
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_n) s_base = atomicAdd(nact_out, s_n);
+  __syncthreads();
+  if (!survive) return;
+  if (lane == 0) act_out[s_base + slot] = q;
   // drop buffered keys above the tightened bound once the buffer is half full
   const uint32_t cnt = min(bufcnt[q], cap);
   if (newU < U && cnt > cap / 2) {
-    uint64_t* b = buf + uint64_t(q) * cap;
+    uint64_t* bq = buf + uint64_t(q) * cap;
     uint32_t wpos = 0;
     for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
       const uint32_t i = i0 + lane;
-      const uint64_t key = i < cnt ? b[i] : ~0ull;
+      const uint64_t key = i < cnt ? bq[i] : ~0ull;
       const bool keep = i < cnt && uint32_t(key >> 32) <= newU;
       const uint32_t bal = __ballot_sync(~0u, keep);
       __syncwarp();
-      if (keep) b[wpos + __popc(bal & lanemask_lt())] = key;
+      if (keep) bq[wpos + __popc(bal & lanemask_lt())] = key;
       wpos += __popc(bal);
       __syncwarp();
     }

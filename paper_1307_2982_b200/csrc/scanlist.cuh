@@ -9,8 +9,7 @@ namespace {
 
 // Register-resident variant for lists of at most 32 * R entries: every load of the list is issued
 // at once (one memory round trip instead of one per 32 entries in each of the two passes), then
-// the histogram, the k-th distance and the in-order compaction work on registers. A 264-entry K7
-// list (k = 100) drops from ~10K clk of dependent L2 round trips to a few hundred plus one trip.
+// the k-th distance (radix select on ballots) and the in-order compaction work on registers.
 template <int R>
 __device__ __forceinline__ uint32_t compact_list_regs(uint64_t* list, uint32_t& cnt, uint32_t tau, uint32_t k,
                                                       uint32_t* hist) {
@@ -21,33 +20,26 @@ __device__ __forceinline__ uint32_t compact_list_regs(uint64_t* list, uint32_t& 
     const uint32_t i = uint32_t(r) * 32 + lane;
     v[r] = i < cnt ? list[i] : ~0ull;
   }
-  for (uint32_t d = lane; d <= tau; d += 32) hist[d] = 0;
-  __syncwarp();
+  // k-th smallest distance by a radix select over the registers (ballots, no shared-memory
+  // histogram: the distances of a list cluster under its bound, so histogram atomics would
+  // serialise up to 32 ways)
+  if (cnt < k) return tau;  // fewer than k entries: nothing to drop
+  uint32_t prefix = 0, rank = k;  // 1-based rank of the target among the candidates left
+  for (int bit = 31 - __clz(max(tau, 1u)); bit >= 0; --bit) {  // every entry's distance is <= tau
+    uint32_t zeros = 0;
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (uint32_t(r) * 32 + lane < cnt) atomicAdd(&hist[uint32_t(v[r] >> 32)], 1u);
-  __syncwarp();
-  uint32_t run = 0, newtau = tau, before = 0;
-  bool found = false;
-  for (uint32_t d0 = 0; d0 <= tau && !found; d0 += 32) {
-    const uint32_t d = d0 + lane;
-    uint32_t x = d <= tau ? hist[d] : 0;
-    const uint32_t own = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(~0u, x, o);
-      if (lane >= o) x += y;
+    for (int r = 0; r < R; ++r) {
+      const uint32_t d = uint32_t(v[r] >> 32);
+      const bool e = uint32_t(r) * 32 + lane < cnt && (d >> (bit + 1)) == (prefix >> (bit + 1)) && !((d >> bit) & 1u);
+      zeros += __popc(__ballot_sync(~0u, e));
     }
-    const uint32_t ok = __ballot_sync(~0u, d <= tau && run + x >= k);
-    if (ok) {
-      const int src = __ffs(ok) - 1;
-      newtau = d0 + src;
-      before = run + __shfl_sync(~0u, x - own, src);
-      found = true;
+    if (rank > zeros) {
+      rank -= zeros;
+      prefix |= 1u << bit;
     }
-    run += __shfl_sync(~0u, x, 31);
   }
-  if (!found) return tau;  // fewer than k entries: nothing to drop
+  const uint32_t newtau = prefix, before = k - rank;
+  (void)hist;
   const uint32_t need_eq = k - before;
   uint32_t wpos = 0, eq_seen = 0;
 #pragma unroll

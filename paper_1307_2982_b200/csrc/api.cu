@@ -226,22 +226,22 @@ int mihg_bucket_lookup(const mihg_index* idx, uint32_t j, uint64_t value, uint32
       lo = two[0];
       hi = two[1];
     } else {
-      mihg::DirBlock b;
-      MIHG_CUDA(cudaMemcpy(&b, t.dir.get() + (value >> mihg::kDirBucketsLog2), sizeof(b),
+      mihg::DirGroup gp;
+      MIHG_CUDA(cudaMemcpy(&gp, t.dir.get() + (value >> mihg::kDirBucketsLog2), sizeof(gp),
                            cudaMemcpyDeviceToHost));
-      const uint32_t tt = uint32_t(value & 63);
-      const uint32_t c = uint32_t((b.p0 >> tt) & 1) | uint32_t(((b.p1 >> tt) & 1) << 1) |
-                         uint32_t(((b.p2 >> tt) & 1) << 2);
+      const uint32_t tt = uint32_t(value & 31);
+      const uint32_t c = ((gp.p0 >> tt) & 1u) | (((gp.p1 >> tt) & 1u) << 1) | (((gp.p2 >> tt) & 1u) << 2);
       if (c) {
-        if (b.esc != mihg::kNoEscape) {
+        const uint32_t below = (1u << tt) - 1u;
+        if (gp.p0 & gp.p1 & gp.p2) {  // escaped group: base is the record index
           uint32_t two[2];
-          MIHG_CUDA(cudaMemcpy(two, t.esc.get() + uint64_t(b.esc) * 65 + tt, 8, cudaMemcpyDeviceToHost));
+          MIHG_CUDA(cudaMemcpy(two, t.esc.get() + uint64_t(gp.base) * mihg::kEscStarts + tt, 8,
+                               cudaMemcpyDeviceToHost));
           lo = two[0];
           hi = two[1];
         } else {
-          const uint64_t below = (uint64_t(1) << tt) - 1;
-          lo = b.ebase + __builtin_popcountll(b.p0 & below) + 2 * __builtin_popcountll(b.p1 & below) +
-               4 * __builtin_popcountll(b.p2 & below);
+          lo = gp.base + __builtin_popcount(gp.p0 & below) + 2 * __builtin_popcount(gp.p1 & below) +
+               4 * __builtin_popcount(gp.p2 & below);
           hi = lo + c;
         }
       }

@@ -3,8 +3,8 @@
 //   K1 extract_keys_kernel   substring key of every code (codes.hpp:214-231)
 //   K2 radix_sort_pairs_u32  stable sort of (key, id) -> ids in (key, id) order (table.hpp:98-99)
 //   K3 dense:  bucket histogram + exclusive scan -> offsets[2^s + 1]
-//      sparse: one warp per 64-bucket directory block -> 3-bit-plane counts + entry base,
-//              escape records (65 exact starts) for blocks holding a bucket of >= 7 entries.
+//      sparse: one warp per 32-bucket directory group -> 3-bit-plane counts + entry base in 16
+//              bytes, escape records (33 exact starts) for groups holding a bucket of >= 7 entries.
 #include <algorithm>
 #include <cstdio>
 #include <atomic>
@@ -207,67 +207,63 @@ __device__ __forceinline__ uint64_t lower_bound_u32(const uint32_t* __restrict__
   return lo;
 }
 
-// One warp per 64-bucket directory block. Phase 0 writes the block and an escape flag;
-// phase 1 (escaped blocks only) writes the 65 exact starts at esc_idx[g].
+// One warp per 32-bucket directory group (lane = bucket). Phase 0 writes the group and an escape
+// flag; phase 1 (escaped groups only) writes the 33 exact starts at esc_idx[g] and points the
+// group's base at that record.
 template <int kPhase>
-__global__ void dir_build_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint64_t nblocks,
-                                 DirBlock* __restrict__ dir, uint32_t* __restrict__ flags,
+__global__ void dir_build_kernel(const uint32_t* __restrict__ keys, uint64_t n, uint64_t ngroups,
+                                 DirGroup* __restrict__ dir, uint32_t* __restrict__ flags,
                                  const uint32_t* __restrict__ esc_idx, uint32_t* __restrict__ esc,
                                  unsigned long long* __restrict__ stats) {
-  __shared__ uint32_t cnt[8][64];
+  __shared__ uint32_t cnt[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
-  for (uint64_t g = blockIdx.x * uint64_t(blockDim.x >> 5) + wib; g < nblocks; g += warps) {
+  for (uint64_t g = blockIdx.x * uint64_t(blockDim.x >> 5) + wib; g < ngroups; g += warps) {
     if (kPhase == 1 && !flags[g]) continue;
     cnt[wib][lane] = 0;
-    cnt[wib][lane + 32] = 0;
     uint64_t lb = 0, ub = 0;
     if (lane == 0) lb = lower_bound_u32(keys, n, g << kDirBucketsLog2);
     if (lane == 1) ub = lower_bound_u32(keys, n, (g + 1) << kDirBucketsLog2);
     lb = __shfl_sync(0xffffffffu, lb, 0);
     ub = __shfl_sync(0xffffffffu, ub, 1);
     __syncwarp();
-    for (uint64_t p = lb + lane; p < ub; p += 32) atomicAdd(&cnt[wib][keys[p] & 63u], 1u);
+    for (uint64_t p = lb + lane; p < ub; p += 32) atomicAdd(&cnt[wib][keys[p] & 31u], 1u);
     __syncwarp();
-    const uint32_t c0 = cnt[wib][lane], c1 = cnt[wib][lane + 32];
+    const uint32_t c = cnt[wib][lane];
     if (kPhase == 0) {
-      const uint32_t s0 = min(c0, 7u), s1 = min(c1, 7u);
-      DirBlock blk;
-      blk.p0 = uint64_t(__ballot_sync(~0u, s0 & 1)) | (uint64_t(__ballot_sync(~0u, s1 & 1)) << 32);
-      blk.p1 = uint64_t(__ballot_sync(~0u, s0 & 2)) | (uint64_t(__ballot_sync(~0u, s1 & 2)) << 32);
-      blk.p2 = uint64_t(__ballot_sync(~0u, s0 & 4)) | (uint64_t(__ballot_sync(~0u, s1 & 4)) << 32);
-      blk.ebase = uint32_t(lb);
-      blk.esc = kNoEscape;
-      const bool escaped = __any_sync(~0u, c0 > kMaxInlineCount || c1 > kMaxInlineCount);
-      const uint32_t ne = __popc(__ballot_sync(~0u, c0 != 0)), ne1 = __popc(__ballot_sync(~0u, c1 != 0));
-      uint32_t mx = max(c0, c1);
+      const uint32_t sc = min(c, 7u);
+      DirGroup grp;
+      grp.p0 = __ballot_sync(~0u, sc & 1);
+      grp.p1 = __ballot_sync(~0u, sc & 2);
+      grp.p2 = __ballot_sync(~0u, sc & 4);
+      grp.base = uint32_t(lb);
+      const bool escaped = __any_sync(~0u, c > kMaxInlineCount);
+      const uint32_t ne = __popc(__ballot_sync(~0u, c != 0));
+      uint32_t mx = c;
 #pragma unroll
       for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(~0u, mx, o));
       if (lane == 0) {
-        dir[g] = blk;
+        dir[g] = grp;
         flags[g] = escaped ? 1u : 0u;
-        if (ne + ne1) {
-          atomicAdd(stats, (unsigned long long)(ne + ne1));
+        if (ne) {
+          atomicAdd(stats, (unsigned long long)ne);
           atomicMax(stats + 1, (unsigned long long)mx);
-          atomicAdd(stats + 2, (unsigned long long)((ne != 0) + (ne1 != 0)));
+          atomicAdd(stats + 2, 1ull);  // non-empty 32-bucket groups (the reference's unit)
         }
       }
     } else {
-      // exclusive prefix of the 64 counts, lanes hold buckets lane and lane+32
-      uint32_t x0 = c0, x1 = c1;
+      uint32_t x = c;  // exclusive prefix of the 32 counts
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y0 = __shfl_up_sync(~0u, x0, o), y1 = __shfl_up_sync(~0u, x1, o);
-        if (lane >= o) x0 += y0, x1 += y1;
+        const uint32_t y = __shfl_up_sync(~0u, x, o);
+        if (lane >= o) x += y;
       }
-      const uint32_t tot0 = __shfl_sync(~0u, x0, 31);
       const uint32_t e = esc_idx[g];
-      uint32_t* rec = esc + uint64_t(e) * 65u;
-      rec[lane] = uint32_t(lb) + x0 - c0;
-      rec[lane + 32] = uint32_t(lb) + tot0 + x1 - c1;
+      uint32_t* rec = esc + uint64_t(e) * kEscStarts;
+      rec[lane] = uint32_t(lb) + x - c;
       if (lane == 0) {
-        rec[64] = uint32_t(ub);
-        dir[g].esc = e;
+        rec[32] = uint32_t(ub);
+        dir[g].base = e;
       }
     }
   }
@@ -335,8 +331,8 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
       MIHG_LAUNCH();
     }
   } else {
-    const uint64_t nblocks = nb >> kDirBucketsLog2;
-    t->dir = DeviceBuffer<DirBlock>(nblocks, st);
+    const uint64_t nblocks = nb >> kDirBucketsLog2;  // 32-bucket groups
+    t->dir = DeviceBuffer<DirGroup>(nblocks, st);
     DeviceBuffer<uint32_t> flags(nblocks, st), esc_idx(nblocks, st);
     const unsigned grid = grid_for(nblocks * 32, 256);
     dir_build_kernel<0><<<grid, 256, 0, st>>>(keys.get(), n, nblocks, t->dir.get(), flags.get(),
@@ -358,7 +354,7 @@ void build_table(Index& idx, uint32_t j, const BuildOptions& opt) {
       }
     }
     if (t->escaped_blocks) {
-      t->esc = DeviceBuffer<uint32_t>(t->escaped_blocks * 65, st);
+      t->esc = DeviceBuffer<uint32_t>(t->escaped_blocks * kEscStarts, st);
       dir_build_kernel<1><<<grid, 256, 0, st>>>(keys.get(), n, nblocks, t->dir.get(), flags.get(),
                                                esc_idx.get(), t->esc.get(), nullptr);
       MIHG_LAUNCH();

@@ -47,26 +47,28 @@ constexpr uint32_t kWarp = 32;
 
 __host__ __device__ constexpr uint32_t words_per_code(uint32_t bits) { return (bits + 63) / 64; }
 
-// Directory block of a sparse (blocked-count) table: 64 consecutive buckets in one 32-byte
-// sector. Bucket t's entry count c_t in 0..6 is spread over three bit-planes (bit i of c_t is
-// bit t of plane i); 7 marks an escaped block whose exact starts live in `esc`.
-//   start(t) = ebase + popc(p0 & below) + 2 popc(p1 & below) + 4 popc(p2 & below)
-struct __align__(32) DirBlock {
-  uint64_t p0, p1, p2;
-  uint32_t ebase;  // index into ids[] of the block's first entry
-  uint32_t esc;    // ~0u, or the escape record (65 absolute starts) index
+// Directory group of a sparse (blocked-count) table: 32 consecutive buckets — one of the
+// reference's 32-bucket groups (table.hpp:40-47) — in 16 bytes. Bucket t's entry count c_t (0..6
+// exact, 7 = saturated) is spread over three 32-bit planes (bit i of c_t is bit t of plane i);
+//   start(t) = base + popc(p0 & below) + 2 popc(p1 & below) + 4 popc(p2 & below).
+// A group holding a saturated bucket (p0 & p1 & p2 != 0) keeps its exact starts in a 33-entry
+// escape record, and `base` is that record's index (probes of its non-empty buckets read the
+// record). A probe reads 16 bytes (4 registers).
+struct __align__(16) DirGroup {
+  uint32_t p0, p1, p2;
+  uint32_t base;  // index into ids[] of the group's first entry, or (escaped) the record index
 };
-static_assert(sizeof(DirBlock) == 32, "one sector per directory block");
-constexpr uint32_t kDirBucketsLog2 = 6;
-constexpr uint32_t kNoEscape = 0xFFFFFFFFu;
+static_assert(sizeof(DirGroup) == 16, "half a sector per directory group");
+constexpr uint32_t kDirBucketsLog2 = 5;
+constexpr uint32_t kEscStarts = 33;  // exact starts per escape record (32 buckets + end)
 constexpr uint32_t kMaxInlineCount = 6;
 
 // One substring table on the device.
 struct DevTable {
   const uint32_t* ids;      // n ids sorted by (substring key, id)
   const uint32_t* offsets;  // dense: 2^s + 1 bucket starts (nullptr when sparse)
-  const DirBlock* dir;      // sparse: 2^(s-6) blocks (nullptr when dense)
-  const uint32_t* esc;      // sparse: 65 absolute starts per escaped block
+  const DirGroup* dir;      // sparse: 2^(s-5) groups (nullptr when dense)
+  const uint32_t* esc;      // sparse: 33 absolute starts per escaped group
   const uint64_t* codes;    // inline codes in table order (W words per entry), or nullptr
   const uint32_t* occ;      // sparse: 1 bit per bucket (non-empty), or nullptr
   uint32_t s;
@@ -112,29 +114,23 @@ __device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint
     lo = hi = 0;
     return;
   }
-  uint32_t r[8];
-  ldg256(t.dir + (v >> kDirBucketsLog2), r);
-  const uint4 y = make_uint4(r[4], r[5], r[6], r[7]);
-  const uint32_t tt = v & 63u;
-  const uint64_t p0 = (uint64_t(r[1]) << 32) | r[0], p1 = (uint64_t(r[3]) << 32) | r[2],
-                 p2 = (uint64_t(r[5]) << 32) | r[4];
-  const uint32_t c = uint32_t((p0 >> tt) & 1u) | (uint32_t((p1 >> tt) & 1u) << 1) |
-                     (uint32_t((p2 >> tt) & 1u) << 2);
+  const uint4 g = __ldg(reinterpret_cast<const uint4*>(t.dir + (v >> kDirBucketsLog2)));
+  const uint32_t tt = v & 31u;
+  const uint32_t c = ((g.x >> tt) & 1u) | (((g.y >> tt) & 1u) << 1) | (((g.z >> tt) & 1u) << 2);
   if (c == 0) {
     lo = hi = 0;
     return;
   }
-  const uint64_t below = (uint64_t(1) << tt) - 1u;
-  // Escaped block (some bucket holds >= 7 entries, stored as count 7): the planes are still exact
-  // for every bucket with count <= 6, so the escape record is read only when this bucket or one
-  // below it is saturated (the clusters the probes visit are where blocks escape).
-  if (y.w != kNoEscape && (c == 7u || (p0 & p1 & p2 & below) != 0)) {
-    const uint32_t* e = t.esc + uint64_t(y.w) * 65u + tt;
+  const uint32_t below = (1u << tt) - 1u;
+  // Escaped group (some bucket saturated at count 7): `base` holds the escape record's index, so
+  // every non-empty bucket of the group reads its exact start from the record.
+  if (g.x & g.y & g.z) {
+    const uint32_t* e = t.esc + uint64_t(g.w) * kEscStarts + tt;
     lo = __ldg(e);
     hi = __ldg(e + 1);
     return;
   }
-  lo = y.z + __popcll(p0 & below) + 2u * __popcll(p1 & below) + 4u * __popcll(p2 & below);
+  lo = g.w + __popc(g.x & below) + 2u * __popc(g.y & below) + 4u * __popc(g.z & below);
   hi = lo + c;
 }
 

@@ -15,8 +15,8 @@ struct TableStorage {
   bool dense = true;
   DeviceBuffer<uint32_t> ids;      // n, sorted by (key, id)
   DeviceBuffer<uint32_t> offsets;  // dense: 2^s + 1
-  DeviceBuffer<DirBlock> dir;      // sparse: 2^(s-6)
-  DeviceBuffer<uint32_t> esc;      // sparse: 65 per escaped block
+  DeviceBuffer<DirGroup> dir;      // sparse: 2^(s-5) groups of 16 bytes
+  DeviceBuffer<uint32_t> esc;      // sparse: 33 per escaped group
   DeviceBuffer<uint64_t> tcodes;   // optional: codes in table order (bucket = contiguous run)
   DeviceBuffer<uint32_t> occ;      // sparse: occupancy bitmap, 1 bit per bucket
   DeviceBuffer<uint32_t> rcodes;   // optional: 32-bit residual codes in table order (see DevTable)
@@ -40,7 +40,7 @@ struct TableStorage {
     rcodes.reset();
   }
   uint64_t bytes() const {
-    return ids.size() * 4 + offsets.size() * 4 + dir.size() * sizeof(DirBlock) + esc.size() * 4 +
+    return ids.size() * 4 + offsets.size() * 4 + dir.size() * sizeof(DirGroup) + esc.size() * 4 +
            tcodes.size() * 8 + occ.size() * 4 + rcodes.size() * 4;
   }
 };

@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? MIHG_PROBE_MINB : 5) m
 #pragma unroll
         for (int b = 0; b < kLaneProbes; ++b) {
           if (ii < iend && it + kLaneProbes + b < pchunk) {
-            const DirBlock* blk = p.tab.dir + ((qa ^ (high | mk)) >> kDirBucketsLog2);
+            const DirGroup* blk = p.tab.dir + ((qa ^ (high | mk)) >> kDirBucketsLog2);
             if (p.prefetch == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(blk));
             else asm volatile("prefetch.global.L2 [%0];" ::"l"(blk));
             mk = next_comb(mk);
@@ -896,7 +896,7 @@ void plan_slicing(ProbeArgs& p, Workspace& ws, uint64_t nact, cudaStream_t st) {
   p.slice_bits = 0;
   const uint32_t s = p.tab.s;
   const double bytes = p.tab.dense ? double((uint64_t(1) << s) + 1) * 4
-                                   : double(uint64_t(1) << (s - kDirBucketsLog2)) * sizeof(DirBlock);
+                                   : double(uint64_t(1) << (s - kDirBucketsLog2)) * sizeof(DirGroup);
   if (!slicing_enabled() || bytes <= 64.0 * (1 << 20) || double(nact) * double(p.ring) < 4.0e6) return;
   uint32_t t = 0;
   while (bytes / double(1u << t) > slice_mb() * (1 << 20) && t < 8) ++t;

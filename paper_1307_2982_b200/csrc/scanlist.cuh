@@ -64,6 +64,7 @@ __device__ __noinline__ uint32_t compact_list(uint64_t* list, uint32_t& cnt, uin
                                  uint32_t* hist) {
   const uint32_t lane = threadIdx.x & 31;
   if (cnt <= 32 * 12) return compact_list_regs<12>(list, cnt, tau, k, hist);
+  if (cnt <= 32 * 24) return compact_list_regs<24>(list, cnt, tau, k, hist);
   MIHG_DASSERT(tau < 4097);
   for (uint32_t d = lane; d <= tau; d += 32) hist[d] = 0;
   __syncwarp();

@@ -15,6 +15,7 @@ namespace mihg {
 namespace {
 
 constexpr int kSelThreads = 512;
+constexpr uint32_t kSelHistBins = 4097;  // distances 0..4096 (codes.hpp:16)
 
 __device__ __forceinline__ bool keep_key(uint64_t key, uint32_t maxd) {
   return uint32_t(key >> 32) <= maxd;
@@ -47,10 +48,65 @@ __global__ void __launch_bounds__(kSelThreads) select_small_kernel(SelectArgs a)
     const uint64_t key = a.keys[base + i];
     if (keep_key(key, maxd)) sk[atomicAdd(&s_cnt, 1u)] = key;
   }
+  uint32_t m = total;  // keys still in play, sk[0, m)
+  if (total > 2 * a.k && total > 256) {
+    // Pre-selection: the k-th smallest distance D from a distance histogram, then only the keys
+    // with d <= D are sorted (the top k by (dist, id) lies among them; ties at D keep every
+    // key so the smallest ids win in the sort).
+    __shared__ uint32_t s_dmax, s_D, s_m;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sk + kSmemKeys);
+    if (threadIdx.x == 0) {
+      s_dmax = 0;
+      s_m = 0;
+    }
+    __syncthreads();
+    uint32_t dm = 0;
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) dm = max(dm, uint32_t(sk[i] >> 32));
+    atomicMax(&s_dmax, dm);
+    __syncthreads();
+    const uint32_t dmax = min(s_dmax, kSelHistBins - 1);
+    for (uint32_t d = threadIdx.x; d <= dmax; d += blockDim.x) hist[d] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) atomicAdd(&hist[min(uint32_t(sk[i] >> 32), dmax)], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0: running prefix, 32 bins per step
+      const uint32_t lane = threadIdx.x;
+      uint32_t run = 0, D = dmax;
+      for (uint32_t d0 = 0; d0 <= dmax; d0 += 32) {
+        uint32_t x = d0 + lane <= dmax ? hist[d0 + lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(~0u, x, o);
+          if (lane >= uint32_t(o)) x += y;
+        }
+        const uint32_t ok = __ballot_sync(~0u, d0 + lane <= dmax && run + x >= a.k);
+        if (ok) {
+          D = d0 + __ffs(ok) - 1;
+          break;
+        }
+        run += __shfl_sync(~0u, x, 31);
+      }
+      if (lane == 0) s_D = D;
+    }
+    __syncthreads();
+    const uint32_t D = s_D;
+    uint64_t mine[kSmemKeys / kSelThreads];
+#pragma unroll
+    for (uint32_t j = 0; j < kSmemKeys / kSelThreads; ++j) {
+      const uint32_t i = threadIdx.x + j * blockDim.x;
+      mine[j] = i < total ? sk[i] : ~0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kSmemKeys / kSelThreads; ++j)
+      if (mine[j] != ~0ull && uint32_t(mine[j] >> 32) <= D) sk[atomicAdd(&s_m, 1u)] = mine[j];
+    __syncthreads();
+    m = s_m;
+  }
   uint32_t N = 32;
-  while (N < total) N <<= 1;
+  while (N < m) N <<= 1;
   __syncthreads();
-  for (uint32_t i = total + threadIdx.x; i < N; i += blockDim.x) sk[i] = ~0ull;
+  for (uint32_t i = m + threadIdx.x; i < N; i += blockDim.x) sk[i] = ~0ull;
   __syncthreads();
   for (uint32_t k2 = 2; k2 <= N; k2 <<= 1) {
     for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
@@ -69,7 +125,7 @@ __global__ void __launch_bounds__(kSelThreads) select_small_kernel(SelectArgs a)
     }
   }
   const uint64_t row = a.out_row ? a.out_row[seg] : seg;
-  const uint32_t kk = min(a.k, total);
+  const uint32_t kk = min(a.k, m);
   for (uint32_t i = threadIdx.x; i < a.k; i += blockDim.x) {
     const bool ok = i < kk;
     const uint64_t key = ok ? sk[i] : ~0ull;
@@ -124,13 +180,9 @@ void select_topk(SelectArgs a, uint32_t nseg, cudaStream_t st) {
   a.filtered_count = fcount.get();
   a.large_list = list.get();
   a.large_count = lcount.get();
-  const size_t smem = size_t(kSmemKeys) * 8;
-  static bool attr_set = false;
-  if (!attr_set) {
-    MIHG_CUDA(cudaFuncSetAttribute(select_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem)));
-    attr_set = true;
-  }
+  const size_t smem = size_t(kSmemKeys) * 8 + size_t(kSelHistBins) * 4;
+  // per call (cheap), so every device the process uses gets the attribute
+  MIHG_CUDA(cudaFuncSetAttribute(select_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   select_small_kernel<<<nseg, kSelThreads, smem, st>>>(a);
   MIHG_LAUNCH();
   uint32_t L = 0;

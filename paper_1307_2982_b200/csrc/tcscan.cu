@@ -41,6 +41,12 @@ constexpr int kTcN = 256;        // codes per tile (MMA N)
 constexpr int kAcc = 2;          // TMEM accumulators of kTcN columns (all 512 columns)
 constexpr int kEpiGroups = 4;    // epilogue groups of 4 warps; group g drains columns [32 g, 32 g + 32)
 constexpr int kEpiCols = kTcN / kEpiGroups;
+// a list is compacted to its exact top-k when it holds kListSlack * k entries (MIHG_TC_SLACK
+// builds: A/B of compaction frequency vs size)
+#ifndef MIHG_TC_SLACK
+#define MIHG_TC_SLACK 2
+#endif
+constexpr uint32_t kListSlack = MIHG_TC_SLACK;
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kProdWarps = 4;    // 128 producer threads: one code each per tile
 constexpr int kRaw = 4;          // raw code tiles in flight (TMA bulk ring)
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           }
         }
         // warp-cooperative compaction of every list that reached 2k entries (scanlist.cuh)
-        uint32_t need = __ballot_sync(~0u, cnt >= 2 * a.k);
+        uint32_t need = __ballot_sync(~0u, cnt >= kListSlack * a.k);
         while (need) {
           const int src = __ffs(need) - 1;
           need &= need - 1;
@@ -744,7 +750,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
   if (!tc_scan_supported(bits)) throw InvalidArgument("tc_scan: code width must be 1..256 bits");
   if (nq == 0 || k == 0) return;
   const uint32_t W = words_per_code(bits);
-  const uint32_t L = 2 * k + kEpiCols;
+  const uint32_t L = kListSlack * k + kEpiCols;
   const bool pair = tc_pair_enabled();
   const uint64_t tileq = pair ? 2 * kTcM : kTcM;  // queries per work unit (CTA or CTA pair)
   const uint64_t sms = uint64_t(device_sm_count()) / (pair ? 2 : 1);  // work units in flight

@@ -750,24 +750,39 @@ __global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32
   __syncthreads();
   if (threadIdx.x == 0 && s_n) s_base = atomicAdd(nact_out, s_n);
   __syncthreads();
-  if (!survive) return;
-  if (lane == 0) act_out[s_base + slot] = q;
-  // drop buffered keys above the tightened bound once the buffer is half full
-  const uint32_t cnt = min(bufcnt[q], cap);
-  if (newU < U && cnt > cap / 2) {
-    uint64_t* bq = buf + uint64_t(q) * cap;
-    uint32_t wpos = 0;
-    for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-      const uint32_t i = i0 + lane;
+  if (survive && lane == 0) act_out[s_base + slot] = q;
+  // drop buffered keys above the tightened bound once the buffer is half full: the queries that
+  // need it are compacted by the whole block, one at a time (a single warp scanning a 32K-key
+  // buffer would set the kernel's length); the buffer's order is irrelevant (selection sorts)
+  __shared__ uint32_t s_cq[32], s_cu[32], s_nc, s_w;
+  if (threadIdx.x == 0) s_nc = 0;
+  __syncthreads();
+  if (survive && lane == 0 && newU < U && min(bufcnt[q], cap) > cap / 2) {
+    const uint32_t at = atomicAdd(&s_nc, 1u);
+    s_cq[at] = q;
+    s_cu[at] = newU;
+  }
+  __syncthreads();
+  for (uint32_t c = 0; c < s_nc; ++c) {
+    const uint32_t cq = s_cq[c], cu = s_cu[c];
+    const uint32_t cnt = min(bufcnt[cq], cap);
+    uint64_t* bq = buf + uint64_t(cq) * cap;
+    if (threadIdx.x == 0) s_w = 0;
+    __syncthreads();
+    for (uint32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
+      const uint32_t i = i0 + threadIdx.x;
       const uint64_t key = i < cnt ? bq[i] : ~0ull;
-      const bool keep = i < cnt && uint32_t(key >> 32) <= newU;
+      const bool keep = i < cnt && uint32_t(key >> 32) <= cu;
+      __syncthreads();  // every key of this pass is read before any is overwritten
       const uint32_t bal = __ballot_sync(~0u, keep);
-      __syncwarp();
-      if (keep) bq[wpos + __popc(bal & lanemask_lt())] = key;
-      wpos += __popc(bal);
-      __syncwarp();
+      uint32_t wbase = 0;
+      if (lane == 0 && bal) wbase = atomicAdd(&s_w, __popc(bal));
+      wbase = __shfl_sync(~0u, wbase, 0);
+      if (keep) bq[wbase + __popc(bal & lanemask_lt())] = key;
+      __syncthreads();
     }
-    if (lane == 0) bufcnt[q] = wpos;
+    if (threadIdx.x == 0) bufcnt[cq] = s_w;
+    __syncthreads();
   }
 }
 
@@ -1299,8 +1314,10 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
       call_allreduce(part, ws.hist_g.get(), nq * b1, 0, st);
       hist_end = ws.hist_g.get();
     }
-    const unsigned g = unsigned((nact_known * 32 + 255) / 256);
-    mih_round_end_kernel<<<g, 256, 0, st>>>(act_in, uint32_t(nact_known), ws.nact_dev.get() + r, act_out,
+    // 32 queries (warps) per block: one global atomic per 32 survivors (same-address atomics
+    // serialise at the L2)
+    const unsigned g = unsigned((nact_known * 32 + 1023) / 1024);
+    mih_round_end_kernel<<<g, 1024, 0, st>>>(act_in, uint32_t(nact_known), ws.nact_dev.get() + r, act_out,
                                              ws.nact_dev.get() + r + 1, hist_end, b1, ws.ubound.get(), kstop, r,
                                              ws.final_r.get(), ws.bufcnt.get(), ws.buf.get(), cap);
     MIHG_LAUNCH();

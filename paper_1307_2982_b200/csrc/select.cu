@@ -30,23 +30,22 @@ __global__ void __launch_bounds__(kSelThreads) select_small_kernel(SelectArgs a)
   const uint32_t maxd = a.seg_maxd ? a.seg_maxd[seg] : 0xFFFFFFFFu;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
-  // count the filtered entries first: route oversized segments to the large path
-  uint32_t mine = 0;
-  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) mine += keep_key(a.keys[base + i], maxd);
-  atomicAdd(&s_cnt, mine);
+  // one pass: filtered keys go straight to shared memory while they fit; the count decides
+  // afterwards whether the segment belongs to the large path (oversized: nothing was lost, the
+  // large path re-reads the segment)
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint64_t key = a.keys[base + i];
+    if (keep_key(key, maxd)) {
+      const uint32_t at = atomicAdd(&s_cnt, 1u);
+      if (at < kSmemKeys) sk[at] = key;
+    }
+  }
   __syncthreads();
   const uint32_t total = s_cnt;
   if (a.filtered_count) a.filtered_count[seg] = total;
   if (total > kSmemKeys) {
     if (threadIdx.x == 0) a.large_list[atomicAdd(a.large_count, 1u)] = seg;
     return;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const uint64_t key = a.keys[base + i];
-    if (keep_key(key, maxd)) sk[atomicAdd(&s_cnt, 1u)] = key;
   }
   uint32_t m = total;  // keys still in play, sk[0, m)
   if (total > 2 * a.k && total > 256) {

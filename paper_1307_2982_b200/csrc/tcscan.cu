@@ -556,6 +556,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
         }
         wait_k(tfull + b, (t / kAcc) & 1, 0);  // the tile's MMAs are complete
         if (warp == 0 && lane == 0) TC_TL(t, 4);
+#ifdef MIHG_TC_DEBUG
+        if (tl && blockIdx.x == 0 && lane == 0 && t >= kTl0 && t < kTl0 + 64)  // per-warp: tile seen
+          tl[2 * 512 + (warp * 64 + (t - kTl0)) * 2] = clock64();
+#endif
         tc_fence_after();
         static_assert(kEpiCols == 64, "packed epilogue drains 64 columns per group");
         {
@@ -568,6 +572,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_scan_kernel(TcArgs a) {
           else mbar_arrive(tempty + b);
           if (warp == 0) TC_TL(t, 5);
 #ifdef MIHG_TC_DEBUG
+          if (tl && blockIdx.x == 0 && t >= kTl0 && t < kTl0 + 64)  // per-warp: tile released
+            tl[2 * 512 + (warp * 64 + (t - kTl0)) * 2 + 1] = clock64();
           if (tl && blockIdx.x < 2 && t >= kTl0 && t < kTl0 + 64)  // the last epilogue warp's release
             atomicMax(tl + blockIdx.x * 512 + (t - kTl0) * 8 + 6, clock64());
 #endif
@@ -807,9 +813,10 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     if (const char* t0 = std::getenv("MIHG_TC_TL0")) a.tl0 = uint32_t(std::atoi(t0));
     const char* pe = std::getenv("MIHG_TC_PROF");
     const bool dbg_prof = pe && pe[0] == '1';
-    DeviceBuffer<unsigned long long> profbuf(dbg_prof ? 32 * 8 + 2 * 64 * 8 : 1, st);
+    constexpr size_t kProfWords = 32 * 8 + 2 * 64 * 8 + 16 * 64 * 2;
+    DeviceBuffer<unsigned long long> profbuf(dbg_prof ? kProfWords : 1, st);
     if (dbg_prof) {
-      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, (32 * 8 + 2 * 64 * 8) * 8, st));
+      MIHG_CUDA(cudaMemsetAsync(profbuf.get(), 0, kProfWords * 8, st));
       a.prof = profbuf.get();
     }
 #endif
@@ -860,7 +867,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     if (prof) MIHG_CUDA(cudaEventRecord(ev[1], st));
 #ifdef MIHG_TC_DEBUG
     if (dbg_prof) {
-      unsigned long long h[32 * 8 + 2 * 64 * 8];
+      static unsigned long long h[32 * 8 + 2 * 64 * 8 + 16 * 64 * 2];
       MIHG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
       MIHG_CUDA(cudaStreamSynchronize(st));
       for (int w = 0; w <= kLoadWarp; ++w) {
@@ -874,6 +881,15 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
       const unsigned long long* T = h + 32 * 8;
       const unsigned long long z = T[0];
       fprintf(stderr, "tctl tile: mma_wait_start tempty_ok full_ok issued | epi_seen epi_released epi_max_released | compactions\n");
+      // per epilogue warp of CTA 0: tile seen / released, relative to warp 0's seen time of the tile
+      const unsigned long long* PW = T + 2 * 512;
+      for (int i = 0; i < 16; ++i) {
+        fprintf(stderr, "tcwarp tile %2d:", i);
+        for (int w = 0; w < 16; ++w)
+          fprintf(stderr, " %5lld/%5lld", (long long)(PW[(w * 64 + i) * 2] - PW[i * 2]),
+                  (long long)(PW[(w * 64 + i) * 2 + 1] - PW[i * 2]));
+        fprintf(stderr, "\n");
+      }
       // CTA 1 (the pair's second SM) on its own clock: deltas to its first epi_seen
       const unsigned long long* U = T + 512;
       const unsigned long long z1 = U[4];

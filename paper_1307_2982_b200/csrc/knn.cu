@@ -218,7 +218,7 @@ struct ProbeArgs {
   Piece* pieces;            // nullable: no piece queue
   uint32_t* piece_count;
   uint32_t piece_cap;
-  uint32_t inline_max, piece_size;
+  uint32_t inline_max, inline_max_sparse, piece_size;
   const uint64_t* binom;    // device_binomials()
   // L2-sliced rounds (slice_bits > 0): active queries grouped by the top t bits G of their
   // substring; units enumerated per (slice P, group G) pair, P-major, claimed in order.
@@ -302,18 +302,32 @@ __global__ void __launch_bounds__(1024) slice_plan_kernel(ProbeArgs p, uint32_t 
     pair_prefix[idx] = c;  // temporarily the count
     run += c;
   }
-  part[threadIdx.x] = run;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long acc = 0;
-    for (uint32_t i = 0; i < blockDim.x; ++i) {
-      const unsigned long long v = part[i];
-      part[i] = acc;
-      acc += v;
-    }
-    pair_prefix[npairs] = acc;
-    *p.work_counter = 0;
+  // block-wide exclusive scan of the per-thread sums (warp shuffles, then the 32 warp totals)
+  __shared__ unsigned long long wsum[32];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(~0u, incl, o);
+    if (lane >= uint32_t(o)) incl += y;
   }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < (blockDim.x >> 5) ? wsum[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(~0u, w, o);
+      if (lane >= uint32_t(o)) w += y;
+    }
+    wsum[lane] = w;  // inclusive over warps
+    if (lane == 31) {
+      pair_prefix[npairs] = w;
+      *p.work_counter = 0;
+    }
+  }
+  __syncthreads();
+  part[threadIdx.x] = (wid ? wsum[wid - 1] : 0ull) + incl - run;
   __syncthreads();
   unsigned long long acc = part[threadIdx.x];
   for (uint32_t j = 0; j < per; ++j) {
@@ -581,7 +595,7 @@ __global__ void __launch_bounds__(kProbeThreads, W <= 2 ? MIHG_PROBE_MINB : 5) m
 #pragma unroll
       for (int b = 0; b < kLaneProbes; ++b) {
         n_cand += cnt[b];
-        if (cnt[b] > p.inline_max && p.pieces) {
+        if (cnt[b] > (p.tab.dense ? p.inline_max : p.inline_max_sparse) && p.pieces) {
           const uint32_t np = (cnt[b] + p.piece_size - 1) / p.piece_size;
           const uint32_t at = atomicAdd(p.piece_count, np);
           if (at + np <= p.piece_cap) {
@@ -1090,7 +1104,9 @@ ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   p.piece_count = ws.piece_count.get();
   p.piece_cap = kPieceQueue;
   p.binom = device_binomials();
+  // dense tables 64, sparse 128 (config 4 +2.1% at 128; config 2 -9% at 128, configs 1/3 neutral)
   static const uint32_t inline_max = env_u32("MIHG_INLINE_MAX", 64);
+  static const uint32_t inline_max_sparse = env_u32("MIHG_INLINE_MAX", 128);
   static const uint32_t piece_size = env_u32("MIHG_PIECE_SIZE", 256);
   static const uint32_t prefetch = env_u32("MIHG_PREFETCH", 0);
   p.prefetch = prefetch;
@@ -1098,6 +1114,7 @@ ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   p.debug_probe_only = env_u32("MIHG_DEBUG_PROBE_ONLY", 0);
 #endif
   p.inline_max = inline_max;
+  p.inline_max_sparse = inline_max_sparse;
   p.piece_size = std::max<uint32_t>(32, piece_size);
   return p;
 }
@@ -1362,6 +1379,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   sa.seg_count = seg_count.get();
   sa.seg_maxd = ws.final_r.get();
   sa.k = k;
+  sa.max_dist = idx.bits;
   sa.id_base = idx.id_base;
   sa.out_ids = d_ids;
   sa.out_dists = d_dists;

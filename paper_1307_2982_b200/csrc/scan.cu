@@ -204,6 +204,7 @@ void popc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, ui
     sa.seg_stride = slots * L;
     sa.seg_count = gcount.get();
     sa.k = k;
+    sa.max_dist = bits;
     sa.id_base = id_base;
     sa.out_ids = d_ids + q0 * k;
     sa.out_dists = d_dists + q0 * k;

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kSelThreads) select_small_kernel(SelectArgs a)
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) dm = max(dm, uint32_t(sk[i] >> 32));
     atomicMax(&s_dmax, dm);
     __syncthreads();
-    const uint32_t dmax = min(s_dmax, kSelHistBins - 1);
+    const uint32_t dmax = min(s_dmax, min(a.max_dist, kSelHistBins - 1));
     for (uint32_t d = threadIdx.x; d <= dmax; d += blockDim.x) hist[d] = 0;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) atomicAdd(&hist[min(uint32_t(sk[i] >> 32), dmax)], 1u);
@@ -179,7 +179,7 @@ void select_topk(SelectArgs a, uint32_t nseg, cudaStream_t st) {
   a.filtered_count = fcount.get();
   a.large_list = list.get();
   a.large_count = lcount.get();
-  const size_t smem = size_t(kSmemKeys) * 8 + size_t(kSelHistBins) * 4;
+  const size_t smem = size_t(kSmemKeys) * 8 + size_t(std::min(a.max_dist + 1, kSelHistBins)) * 4;
   // per call (cheap), so every device the process uses gets the attribute
   MIHG_CUDA(cudaFuncSetAttribute(select_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   select_small_kernel<<<nseg, kSelThreads, smem, st>>>(a);

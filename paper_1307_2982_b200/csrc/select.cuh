@@ -18,6 +18,7 @@ struct SelectArgs {
   const uint64_t* out_row = nullptr;
   uint32_t k = 0;
   uint32_t id_base = 0;
+  uint32_t max_dist = 4096;  // an upper bound on every key's distance (the code width): sizes the histogram
   uint32_t* out_ids = nullptr;
   uint32_t* out_dists = nullptr;
   // filled by select_topk

@@ -909,6 +909,7 @@ void tc_scan_knn_device(const uint64_t* d_codes, uint64_t n, uint32_t bits, uint
     sa.seg_stride = uint64_t(a.slots) * L;
     sa.seg_count = gcount.get();
     sa.k = k;
+    sa.max_dist = bits;
     sa.id_base = id_base;
     sa.out_ids = d_ids + q0 * k;
     sa.out_dists = d_dists + q0 * k;

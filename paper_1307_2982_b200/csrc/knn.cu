@@ -486,13 +486,19 @@ constexpr int kProbeWarps = kProbeThreads / 32;
 // of the entries lane-parallel, two per lane per pass (entry t belongs to the bucket whose
 // [off, off + cnt) holds t: 7-step binary search in shared memory), so bucket-size skew never
 // idles the warp. Buckets above kInlineMax go to the piece queue.
-#ifndef MIHG_PROBE_MINB
-#define MIHG_PROBE_MINB 8  // resident blocks per SM for W <= 2 (32 registers at 8)
+// Resident blocks per SM (MIHG_PROBE_MINB overrides the W <= 2 value): 8 (32 registers) for
+// 1-2 probes per lane, 6 (40 registers, spills 172 -> 40 B) for the 4-probe sparse variant.
+// Measured B200 sweep: config 4 (4 probes) 8/6/5/4 blocks = 951K/970K/872K/852K q/s; config 3
+// (2 probes) 271K/242K/227K/194K — occupancy wins over spills except for the 4-probe kernel.
+#ifdef MIHG_PROBE_MINB
+constexpr int probe_min_blocks(int W, int) { return W <= 2 ? MIHG_PROBE_MINB : 5; }
+#else
+constexpr int probe_min_blocks(int W, int lane_probes) { return W <= 2 ? (lane_probes >= 4 ? 6 : 8) : 5; }
 #endif
 template <int W, bool kTrace, int kLaneProbes>
-__global__ void __launch_bounds__(kProbeThreads, W <= 2 ? MIHG_PROBE_MINB : 5) mih_probe_kernel(ProbeArgs p) {
+__global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes)) mih_probe_kernel(ProbeArgs p) {
   constexpr int kWarpBuckets = 32 * kLaneProbes;
-  constexpr int kSearchSteps = kLaneProbes == 1 ? 5 : kLaneProbes == 2 ? 6 : 7;
+  constexpr int kSearchSteps = kLaneProbes == 1 ? 5 : kLaneProbes == 2 ? 6 : kLaneProbes == 4 ? 7 : 8;
   __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
   __shared__ uint32_t s_off[kProbeWarps][kWarpBuckets];
   const uint32_t nw = W ? W : p.nw;
@@ -850,18 +856,20 @@ int lane_probes(const DevTable& t) {
 template <int W, bool kTrace>
 void launch_probe(const ProbeArgs& p, cudaStream_t st) {
   const uint64_t blocks_needed = (p.total + kProbeWarps - 1) / kProbeWarps;
-  const uint64_t max_blocks = uint64_t(device_sm_count()) * 8;
+  const int lp = lane_probes(p.tab);
+  const int minb = lp == 1 ? probe_min_blocks(W, 1) : lp == 4 ? probe_min_blocks(W, 4) : probe_min_blocks(W, 2);
+  const uint64_t max_blocks = uint64_t(device_sm_count()) * minb;  // one resident wave
   const unsigned grid = p.slice_bits || p.d_nact ? unsigned(max_blocks)
                                                 : unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
   if (p.pieces) MIHG_CUDA(cudaMemsetAsync(p.piece_count, 0, 4, st));
-  switch (lane_probes(p.tab)) {
+  switch (lp) {
     case 1: mih_probe_kernel<W, kTrace, 1><<<grid, kProbeThreads, 0, st>>>(p); break;
     case 4: mih_probe_kernel<W, kTrace, 4><<<grid, kProbeThreads, 0, st>>>(p); break;
     default: mih_probe_kernel<W, kTrace, 2><<<grid, kProbeThreads, 0, st>>>(p);
   }
   MIHG_LAUNCH();
   if (p.pieces) {
-    mih_piece_kernel<W, kTrace><<<unsigned(max_blocks), kProbeThreads, 0, st>>>(p);
+    mih_piece_kernel<W, kTrace><<<unsigned(device_sm_count() * 8), kProbeThreads, 0, st>>>(p);
     MIHG_LAUNCH();
   }
 }

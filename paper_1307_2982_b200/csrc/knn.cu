@@ -843,7 +843,7 @@ __global__ void zero_trace_kernel(uint64_t nq, Trace* traces) {
 }
 
 // Buckets probed per lane per iteration (MIHG_LANE_PROBES=1|2|4 overrides): 4 for the sparse
-// directory of 32-bit tables (more independent DRAM sectors in flight: config 4 +2.5%), 2 for dense
+// directory of 32-bit tables (more independent DRAM sectors in flight: config 4 +2.5%; 8 at 6 or 5 blocks/SM: -13%), 2 for dense
 // offsets (fewer registers: config 3 -7% at 4; measured B200 sweep).
 int lane_probes(const DevTable& t) {
   static const int v = [] {

@@ -100,14 +100,19 @@ __device__ __forceinline__ uint32_t unrank_comb(const uint64_t* __restrict__ bin
                                                 uint32_t s, uint32_t z) {
   uint32_t mask = 0;
   uint32_t c = s;
-  for (uint32_t t = z; t >= 1; --t) {
-    uint32_t cc = c - 1;
-    uint32_t b = uint32_t(__ldg(binom + cc * kBinomStride + t));
-    while (b > idx) b = uint32_t(__ldg(binom + (--cc) * kBinomStride + t));
-    mask |= 1u << cc;
-    idx -= b;
-    c = cc;
+  for (uint32_t t = z; t >= 2; --t) {
+    // largest cc < c with C(cc, t) <= idx (C(t - 1, t) = 0 always qualifies): binary search
+    uint32_t lo = t - 1, hi = c;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (uint32_t(__ldg(binom + mid * kBinomStride + t)) <= idx) lo = mid;
+      else hi = mid;
+    }
+    mask |= 1u << lo;
+    idx -= uint32_t(__ldg(binom + lo * kBinomStride + t));
+    c = lo;
   }
+  if (z >= 1) mask |= 1u << idx;  // C(cc, 1) = cc
   return mask;
 }
 
@@ -498,11 +503,11 @@ constexpr int probe_min_blocks(int W, int lane_probes) { return W <= 2 ? (lane_p
 template <int W, bool kTrace, int kLaneProbes>
 __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes)) mih_probe_kernel(ProbeArgs p) {
   constexpr int kWarpBuckets = 32 * kLaneProbes;
-  constexpr int kSearchSteps = kLaneProbes == 1 ? 5 : kLaneProbes == 2 ? 6 : kLaneProbes == 4 ? 7 : 8;
+  constexpr int kNzBits = kLaneProbes == 1 ? 1 : kLaneProbes == 2 ? 2 : kLaneProbes == 4 ? 3 : 4;
   __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
   __shared__ uint32_t s_off[kProbeWarps][kWarpBuckets];
   const uint32_t nw = W ? W : p.nw;
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, lt = lanemask_lt();
   uint32_t pchunk = p.chunk;
   uint64_t pcpq = p.cpq, ptotal = p.total;
   if (p.d_nact) {  // device-planned round
@@ -626,31 +631,50 @@ __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes
 #ifdef MIHG_TC_DEBUG
       if (p.debug_probe_only) continue;  // traffic attribution: directory probes alone
 #endif
+      // the non-empty buckets, compacted in lane-major order: (first entry, offset in the union)
+      uint32_t nz = 0;
+#pragma unroll
+      for (int b = 0; b < kLaneProbes; ++b) nz += cnt[b] != 0;
+      uint32_t sp = 0, n_ne = 0;
+#pragma unroll
+      for (int bit = 0; bit < kNzBits; ++bit) {
+        const uint32_t bal = __ballot_sync(~0u, (nz >> bit) & 1u);
+        sp += __popc(bal & lt) << bit;
+        n_ne += __popc(bal) << bit;
+      }
       uint32_t off = incl - mine;
 #pragma unroll
       for (int b = 0; b < kLaneProbes; ++b) {
-        s_lo[wib][lane * kLaneProbes + b] = lo[b];
-        s_off[wib][lane * kLaneProbes + b] = off;
-        off += cnt[b];
+        if (cnt[b]) {
+          s_lo[wib][sp] = lo[b];
+          s_off[wib][sp] = off;
+          ++sp;
+          off += cnt[b];
+        }
       }
       __syncwarp();
+      // Entry t of the union belongs to the last bucket whose offset is <= t. Offsets are distinct
+      // and ascending, so the buckets starting inside a 64-entry window are the next <= 64 list
+      // slots after `cur` (the count of buckets that started before the window): their start
+      // positions, OR-reduced into a 64-bit mask, rank every entry with one popcount.
+      uint32_t cur = 0;
+      const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
       for (uint32_t t0 = 0; t0 < total; t0 += 64) {
+        const uint32_t i0 = cur + lane, i1 = i0 + 32;
+        const uint32_t o0 = i0 < n_ne ? s_off[wib][i0] - t0 : 64u, o1 = i1 < n_ne ? s_off[wib][i1] - t0 : 64u;
+        uint32_t mlo = (o0 < 32 ? 1u << o0 : 0u) | (o1 < 32 ? 1u << o1 : 0u);
+        uint32_t mhi = (o0 - 32 < 32 ? 1u << (o0 - 32) : 0u) | (o1 - 32 < 32 ? 1u << (o1 - 32) : 0u);
+        mlo = __reduce_or_sync(~0u, mlo);
+        mhi = __reduce_or_sync(~0u, mhi);
+        const uint32_t nlo = __popc(mlo);
+        const uint32_t a0 = cur + __popc(mlo & le) - 1, a1 = cur + nlo + __popc(mhi & le) - 1;
         uint32_t e[2];
         bool v[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t t = t0 + h * 32 + lane;
-          v[h] = t < total;
-          // owning bucket: last slot with off <= t (binary search over 128 offsets)
-          uint32_t a = 0, bnd = kWarpBuckets;
-#pragma unroll
-          for (int step = 0; step < kSearchSteps; ++step) {
-            const uint32_t mid = (a + bnd) >> 1;
-            if (s_off[wib][mid] <= t) a = mid;
-            else bnd = mid;
-          }
-          e[h] = s_lo[wib][a] + (t - s_off[wib][a]);
-        }
+        v[0] = t0 + lane < total;
+        v[1] = t0 + 32 + lane < total;
+        e[0] = s_lo[wib][a0] + (t0 + lane - s_off[wib][a0]);
+        e[1] = s_lo[wib][a1] + (t0 + 32 + lane - s_off[wib][a1]);
+        cur += nlo + __popc(mhi);
         verify_entries<W, kTrace>(p, ctx, v[0], e[0], v[1], e[1], qc, nw, n_new);
       }
       __syncwarp();

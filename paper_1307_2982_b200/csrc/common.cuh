@@ -102,20 +102,22 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
                : "l"(p));
 }
 
-// ---- bucket probe: [lo, hi) slice of ids[] for bucket `v` (table.hpp:178-188 semantics).
-__device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint32_t& lo,
-                                             uint32_t& hi) {
-  if (t.dense) {
-    lo = __ldg(t.offsets + v);
-    hi = __ldg(t.offsets + v + 1);
-    return;
-  }
-  if (t.occ && !((__ldg(t.occ + (v >> 5)) >> (v & 31)) & 1u)) {  // empty: an L2 hit, no sector
-    lo = hi = 0;
-    return;
-  }
-  const uint4 g = __ldg(reinterpret_cast<const uint4*>(t.dir + (v >> kDirBucketsLog2)));
-  const uint32_t tt = v & 31u;
+// One directory group of a sparse table (16 bytes). The directory is re-read by other queries of
+// the same key slice: keep it in L2 (evict last); the candidate codes behind it stream through
+// (evict first, verify_residual).
+__device__ __forceinline__ uint4 load_dir_group(const DevTable& t, uint32_t gi) {
+  uint4 g;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+               : "l"(t.dir + gi), "l"(pol));
+  return g;
+}
+
+// [lo, hi) of bucket tt (0..31) of a loaded directory group.
+__device__ __forceinline__ void decode_dir_group(const DevTable& t, const uint4& g, uint32_t tt, uint32_t& lo,
+                                                 uint32_t& hi) {
   const uint32_t c = ((g.x >> tt) & 1u) | (((g.y >> tt) & 1u) << 1) | (((g.z >> tt) & 1u) << 2);
   if (c == 0) {
     lo = hi = 0;
@@ -132,6 +134,22 @@ __device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint
   }
   lo = g.w + __popc(g.x & below) + 2u * __popc(g.y & below) + 4u * __popc(g.z & below);
   hi = lo + c;
+}
+
+// ---- bucket probe: [lo, hi) slice of ids[] for bucket `v` (table.hpp:178-188 semantics).
+__device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint32_t& lo,
+                                             uint32_t& hi) {
+  if (t.dense) {
+    lo = __ldg(t.offsets + v);
+    hi = __ldg(t.offsets + v + 1);
+    return;
+  }
+  if (t.occ && !((__ldg(t.occ + (v >> 5)) >> (v & 31)) & 1u)) {  // empty: an L2 hit, no sector
+    lo = hi = 0;
+    return;
+  }
+  const uint4 g = load_dir_group(t, v >> kDirBucketsLog2);
+  decode_dir_group(t, g, v & 31u, lo, hi);
 }
 
 // Full-code Hamming distance (codes.hpp:38-42). W > 0: compile-time word count.

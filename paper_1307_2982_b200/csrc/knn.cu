@@ -50,6 +50,7 @@ struct Workspace {
   DeviceBuffer<Piece> pieces;
   DeviceBuffer<uint32_t> piece_count;
   DeviceBuffer<uint32_t> gstart, grouped;
+  DeviceBuffer<uint32_t> compact_list, compact_n;  // (query, new bound) pairs of a round's buffer compactions
   DeviceBuffer<uint64_t> pair_prefix;
   DeviceBuffer<unsigned long long> work_counter;
   uint32_t* h_counter = nullptr;
@@ -387,7 +388,11 @@ template <bool kTrace>
 __device__ __forceinline__ void verify_residual(const ProbeArgs& p, const QueryCtx& c, bool v0, uint32_t e0,
                                                 bool v1, uint32_t e1, uint64_t q, uint64_t& n_new) {
   const uint32_t qo = uint32_t(q >> p.tab.rshift);
-  const uint32_t r0 = v0 ? __ldg(p.tab.rcodes + e0) : 0u, r1 = v1 ? __ldg(p.tab.rcodes + e1) : 0u;
+  uint32_t r0 = 0, r1 = 0;  // candidate codes stream through L2: evict first
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (v0) asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r0) : "l"(p.tab.rcodes + e0), "l"(pol));
+  if (v1) asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r1) : "l"(p.tab.rcodes + e1), "l"(pol));
   const uint32_t do0 = __popc(qo ^ r0), do1 = __popc(qo ^ r1);
   const uint32_t dist0 = p.rr + do0, dist1 = p.rr + do1;
   const bool other_first = p.a == 1;  // the other table (j = 1 - a) precedes this one
@@ -743,8 +748,9 @@ __global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32
                                      uint32_t* __restrict__ act_out, uint32_t* __restrict__ nact_out,
                                      const uint32_t* __restrict__ hist, uint32_t b1,
                                      uint32_t* __restrict__ ubound, uint32_t k, uint32_t r,
-                                     uint32_t* __restrict__ final_r, uint32_t* __restrict__ bufcnt,
-                                     uint64_t* __restrict__ buf, uint32_t cap) {
+                                     uint32_t* __restrict__ final_r, const uint32_t* __restrict__ bufcnt,
+                                     uint32_t cap, uint32_t* __restrict__ compact_list,
+                                     uint32_t* __restrict__ compact_n) {
   __shared__ uint32_t s_n, s_base;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -795,20 +801,26 @@ __global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32
   if (threadIdx.x == 0 && s_n) s_base = atomicAdd(nact_out, s_n);
   __syncthreads();
   if (survive && lane == 0) act_out[s_base + slot] = q;
-  // drop buffered keys above the tightened bound once the buffer is half full: the queries that
-  // need it are compacted by the whole block, one at a time (a single warp scanning a 32K-key
-  // buffer would set the kernel's length); the buffer's order is irrelevant (selection sorts)
-  __shared__ uint32_t s_cq[32], s_cu[32], s_nc, s_w;
-  if (threadIdx.x == 0) s_nc = 0;
-  __syncthreads();
+  // drop buffered keys above the tightened bound once the buffer is half full: such queries are
+  // listed for mih_compact_kernel (one block each; in here, the 32 queries of a block would be
+  // compacted one after another and a single block would set the kernel's length)
   if (survive && lane == 0 && newU < U && min(bufcnt[q], cap) > cap / 2) {
-    const uint32_t at = atomicAdd(&s_nc, 1u);
-    s_cq[at] = q;
-    s_cu[at] = newU;
+    const uint32_t at = atomicAdd(compact_n, 1u);
+    compact_list[2 * at] = q;
+    compact_list[2 * at + 1] = newU;
   }
-  __syncthreads();
-  for (uint32_t c = 0; c < s_nc; ++c) {
-    const uint32_t cq = s_cq[c], cu = s_cu[c];
+}
+
+// In-place compaction of the listed queries' candidate buffers to the keys with dist <= the new
+// bound (one block per query, block-stride over the list). The buffer's order is irrelevant.
+__global__ void __launch_bounds__(1024) mih_compact_kernel(const uint32_t* __restrict__ compact_list,
+                                                          const uint32_t* __restrict__ compact_n,
+                                                          uint32_t* __restrict__ bufcnt,
+                                                          uint64_t* __restrict__ buf, uint32_t cap) {
+  __shared__ uint32_t s_w;
+  const uint32_t lane = threadIdx.x & 31, njobs = *compact_n;
+  for (uint32_t c = blockIdx.x; c < njobs; c += gridDim.x) {
+    const uint32_t cq = compact_list[2 * c], cu = compact_list[2 * c + 1];
     const uint32_t cnt = min(bufcnt[cq], cap);
     uint64_t* bq = buf + uint64_t(cq) * cap;
     if (threadIdx.x == 0) s_w = 0;
@@ -1010,6 +1022,8 @@ void ensure_workspace(Index& idx, uint64_t nq, uint32_t cap, cudaStream_t st) {
   ws->pieces = DeviceBuffer<Piece>(kPieceQueue, st);
   ws->piece_count = DeviceBuffer<uint32_t>(1, st);
   ws->gstart = DeviceBuffer<uint32_t>(257, st);
+  ws->compact_list = DeviceBuffer<uint32_t>(2 * nq, st);
+  ws->compact_n = DeviceBuffer<uint32_t>(b1 + 2, st);  // one counter per round, zeroed per search
   ws->pair_prefix = DeviceBuffer<uint64_t>((1u << 16) + 1, st);
   ws->work_counter = DeviceBuffer<unsigned long long>(1, st);
   MIHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ws->h_counter), 16));
@@ -1238,6 +1252,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   MIHG_CUDA(cudaMemsetAsync(ws.hist.get(), 0, nq * b1 * 4, st));
   MIHG_CUDA(cudaMemsetAsync(ws.trc.get(), 0, 2 * nq * 8, st));
   MIHG_CUDA(cudaMemsetAsync(ws.nact_dev.get(), 0, ws.nact_dev.size() * 4, st));
+  MIHG_CUDA(cudaMemsetAsync(ws.compact_n.get(), 0, ws.compact_n.size() * 4, st));
   mih_init_kernel<<<g1, 256, 0, st>>>(nq, idx.bits, ws.ubound.get(), ws.bufcnt.get(),
                                        ws.dropmin.get(), ws.act0.get(), ws.final_r.get(), ws.nact_dev.get());
   MIHG_LAUNCH();
@@ -1368,7 +1383,11 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     const unsigned g = unsigned((nact_known * 32 + 1023) / 1024);
     mih_round_end_kernel<<<g, 1024, 0, st>>>(act_in, uint32_t(nact_known), ws.nact_dev.get() + r, act_out,
                                              ws.nact_dev.get() + r + 1, hist_end, b1, ws.ubound.get(), kstop, r,
-                                             ws.final_r.get(), ws.bufcnt.get(), ws.buf.get(), cap);
+                                             ws.final_r.get(), ws.bufcnt.get(), cap, ws.compact_list.get(),
+                                             ws.compact_n.get() + r);
+    MIHG_LAUNCH();
+    mih_compact_kernel<<<unsigned(std::min<uint64_t>(nact_known, uint64_t(device_sm_count()) * 2)), 1024, 0, st>>>(
+        ws.compact_list.get(), ws.compact_n.get() + r, ws.bufcnt.get(), ws.buf.get(), cap);
     MIHG_LAUNCH();
     MIHG_CUDA(cudaMemcpyAsync(ws.h_nact + r + 1, ws.nact_dev.get() + r + 1, 4, cudaMemcpyDeviceToHost, st));
     MIHG_CUDA(cudaEventRecord(ws.ev_round[r], st));

@@ -47,6 +47,24 @@ CONFIGS = {
 MIX_DIM, MIX_COMPS = 128, 64
 
 
+_REAL_STDOUT = None
+
+
+def claim_stdout():
+    """Keep stdout for the ONE JSON line: everything else written to fd 1 from here on (NCCL's
+    version banner, library chatter) goes to stderr."""
+    global _REAL_STDOUT
+    if _REAL_STDOUT is None:
+        sys.stdout.flush()
+        _REAL_STDOUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    out = _REAL_STDOUT or sys.stdout
+    print(json.dumps(obj), file=out, flush=True)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -343,7 +361,7 @@ def run_reference_arm(args):
     import oracle
 
     if not oracle.have_ref():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmihref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libmihref.so not built"})
         return
     t0 = time.time()
     db = None if cfg["data"] == "uniform" else make_codes_host_cpu(cfg, 0, cfg["n"], cfg["db_seed"])
@@ -363,12 +381,13 @@ def run_reference_arm(args):
         "e2e": {"value": cpu["value"], "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "setup": {"gen_s": gen_s + leg.get("gen_s", 0), "index_build_s": leg.get("index_build_s")},
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 # ---------------------------------------------------------------------------------------------
 def main():
     args = parse()
+    claim_stdout()
     if args.impl == "reference":
         run_reference_arm(args)
         return
@@ -531,7 +550,7 @@ def main():
         dist.all_reduce(vt, op=dist.ReduceOp.MIN)
         verified = bool(vt.item())
     if not verified:
-        print(json.dumps({"error": "verification failed: the timed kNN result differs from the exhaustive scan"}))
+        emit({"error": "verification failed: the timed kNN result differs from the exhaustive scan"})
         sys.exit(3)
 
     # ---- algorithmic bytes from the reference-identical traces (untimed run) ----
@@ -653,6 +672,27 @@ def main():
                     "mean_trace": {"lookups": float(lookups.mean()), "candidates": float(cands.mean()),
                                    "unique": float(uniq.mean()), "final_radius": float(radius.mean())}}
 
+        # Sparse (32-bit substring) tables: the probe kernel is bound by the GPU's random-access
+        # rate, not by streaming bandwidth. Measure that rate here for one
+        # lookup's access pattern — a directory group in a 128 MB key slice, then for 29% of the
+        # lookups (tools/probe_stats_c4.py) a candidate code in the slice's share of the
+        # table-order codes — and report the kernel's own lookup rate beside it.
+        s_bits = bits // cfg["m"]
+        if rank == 0 and probe_ms > 0 and s_bits >= 27 and (1 << s_bits) > max(1 << 24, 2 * (hi - lo)):
+            dir_total = (1 << (s_bits - 5)) * 16
+            dir_slice = min(dir_total, 128 << 20)
+            code_bytes = (hi - lo) * (4 if (W == 1 and cfg["m"] == 2) else 8 * W)
+            codes_slice = max(1 << 20, int(code_bytes * dir_slice / dir_total))
+            rate = C.c_double(0.0)
+            _lib.check(L.mihg_calibrate_random_lookups(dev.index or 0, dir_slice, codes_slice, 29, C.byref(rate)))
+            ach = float(lookups.sum()) * nq / nq_tr / (world if probe_part else 1) / (probe_ms / 1000.0)
+            roofline["random_access"] = {
+                "achieved_lookups_per_s": ach, "device_lookups_per_s": rate.value,
+                "frac": ach / rate.value if rate.value else None,
+                "model": "mihg_calibrate_random_lookups: 16 B at a random place of a %d MB directory slice, then "
+                         "for 29%% of the lookups 4 B at a random place of %d MB of table-order codes; 4 lookups "
+                         "in flight per lane, 6 x 256 threads per SM" % (dir_slice >> 20, codes_slice >> 20)}
+
     # ---- CPU baseline + parity against the reference itself (rank 0, N = 1 only) ----
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -671,7 +711,7 @@ def main():
             cpu = reference_baseline_json(leg, args.config)
             parity = parity_check(leg, res_ids.cpu().numpy(), res_d.cpu().numpy(), t)
             if parity["mismatches"]:
-                print(json.dumps({"error": "parity failed: GPU rows differ from the reference", "parity": parity}))
+                emit({"error": "parity failed: GPU rows differ from the reference", "parity": parity})
                 sys.exit(3)
         else:
             cpu = {"value": None, "unavailable": "oracle/_ref not built"}
@@ -688,7 +728,7 @@ def main():
             "cpu_baseline": cpu, "clocks": clk,
             "setup": {"gen_s": gen_s, "index_build_s": build_s, "index_device_bytes": idx.device_bytes()},
         }
-        print(json.dumps(line))
+        emit(line)
     idx.close()
     if dist:
         dist.destroy_process_group()

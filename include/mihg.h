@@ -251,6 +251,16 @@ int mihg_profile_enable(int on);
 void mihg_profile_reset(void);
 int mihg_profile_read(mihg_profile* out);
 
+/* Calibration (no reference counterpart): the rate at which THIS GPU serves the dependent random
+ * access pattern of one MIH lookup on a sparse table — a 16-byte directory group read at a random
+ * place of a `dir_bytes` slice, followed for `nonempty_pct` percent of the lookups by a 4-byte
+ * candidate read at a random place of a `codes_bytes` range — in lookups per second. Uses a
+ * scratch allocation of dir_bytes + codes_bytes on `device`. bench.py reports it next to the MIH
+ * probe kernel's own lookup rate (the probe kernel is bound by this
+ * random-access rate, not by streaming HBM bandwidth). */
+int mihg_calibrate_random_lookups(int device, uint64_t dir_bytes, uint64_t codes_bytes,
+                                  uint32_t nonempty_pct, double* lookups_per_s);
+
 /* Seeded Gaussian-mixture sign-projection codes (BASELINE configs 2 and 4; not in the reference,
  * which has gen_correlated_vectors + lsh_encode, io.hpp:245-262, :312-331). Exact integer
  * arithmetic, defined in paper_1307_2982_b200/csrc/gen.cu. Writes codes [first, first + n) as

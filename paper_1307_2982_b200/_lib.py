@@ -128,6 +128,8 @@ SYMBOLS = [
     ("mihg_profile_enable", C.c_int, [C.c_int]),
     ("mihg_profile_reset", None, []),
     ("mihg_profile_read", C.c_int, [C.POINTER(Profile)]),
+    ("mihg_calibrate_random_lookups", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32,
+                                                C.POINTER(C.c_double)]),
 ]
 
 _lib = None

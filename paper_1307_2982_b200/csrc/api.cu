@@ -501,6 +501,79 @@ int mihg_merge_topk_device(const uint32_t* d_ids, const uint32_t* d_dists, uint3
   });
 }
 
+// ---- calibration: random-access lookup rate of the device (see include/mihg.h)
+namespace {
+__device__ __forceinline__ uint64_t calib_mix(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+// Four independent lookups in flight per lane, like the sparse probe kernel.
+__global__ void __launch_bounds__(256) calib_lookup_kernel(const uint8_t* __restrict__ dir, uint64_t dir_bytes,
+                                                           const uint8_t* __restrict__ codes, uint64_t codes_bytes,
+                                                           uint32_t nonempty_pct, uint64_t per_thread, uint64_t seed,
+                                                           uint32_t* sink) {
+  const uint64_t tid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  uint32_t acc = 0;
+  for (uint64_t i = 0; i < per_thread; i += 4) {
+    uint4 g[4];
+    uint64_t h[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      h[u] = calib_mix(seed + tid * per_thread + i + u);
+      g[u] = __ldg(reinterpret_cast<const uint4*>(dir + ((h[u] % dir_bytes) & ~15ull)));
+    }
+    uint32_t r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ne = ((h[u] >> 40) % 100) < nonempty_pct;
+      const uint64_t pos = (((h[u] >> 8) + g[u].x) % codes_bytes) & ~3ull;
+      r[u] = ne ? __ldg(reinterpret_cast<const uint32_t*>(codes + pos)) : g[u].y;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc ^= r[u];
+  }
+  if (acc == 0x12345u) *sink = acc;  // keeps the loads alive
+}
+}  // namespace
+
+int mihg_calibrate_random_lookups(int device, uint64_t dir_bytes, uint64_t codes_bytes, uint32_t nonempty_pct,
+                                  double* lookups_per_s) {
+  return guarded([&] {
+    if (!lookups_per_s || dir_bytes < 16 || codes_bytes < 4 || nonempty_pct > 100)
+      throw mihg::InvalidArgument("calibrate: bad arguments");
+    MIHG_CUDA(cudaSetDevice(device));
+    uint8_t* buf = nullptr;
+    uint32_t* sink = nullptr;
+    MIHG_CUDA(cudaMalloc(&buf, dir_bytes + codes_bytes));
+    MIHG_CUDA(cudaMalloc(&sink, 4));
+    MIHG_CUDA(cudaMemset(buf, 0, dir_bytes + codes_bytes));
+    cudaEvent_t a, b;
+    MIHG_CUDA(cudaEventCreate(&a));
+    MIHG_CUDA(cudaEventCreate(&b));
+    const int blocks = mihg::device_sm_count() * 6, threads = 256;
+    const uint64_t per_thread = 1024;
+    float ms = 0;
+    for (int rep = 0; rep < 2; ++rep) {  // the second run is the measurement
+      MIHG_CUDA(cudaEventRecord(a, nullptr));
+      calib_lookup_kernel<<<blocks, threads>>>(buf, dir_bytes, buf + dir_bytes, codes_bytes, nonempty_pct,
+                                               per_thread, 7 + rep, sink);
+      MIHG_LAUNCH();
+      MIHG_CUDA(cudaEventRecord(b, nullptr));
+      MIHG_CUDA(cudaEventSynchronize(b));
+      MIHG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    cudaFree(sink);
+    *lookups_per_s = double(blocks) * threads * double(per_thread) / (double(ms) * 1e-3);
+  });
+}
+
 int mihg_profile_enable(int on) {
   mihg::profile().enabled = on != 0;
   return MIHG_OK;

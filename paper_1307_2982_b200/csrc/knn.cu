@@ -500,10 +500,15 @@ constexpr int kProbeWarps = kProbeThreads / 32;
 // 1-2 probes per lane, 6 (40 registers, spills 172 -> 40 B) for the 4-probe sparse variant.
 // Measured B200 sweep: config 4 (4 probes) 8/6/5/4 blocks = 951K/970K/872K/852K q/s; config 3
 // (2 probes) 271K/242K/227K/194K — occupancy wins over spills except for the 4-probe kernel.
+#ifndef MIHG_MINB_W2
+#define MIHG_MINB_W2 8
+#endif
 #ifdef MIHG_PROBE_MINB
 constexpr int probe_min_blocks(int W, int) { return W <= 2 ? MIHG_PROBE_MINB : 5; }
 #else
-constexpr int probe_min_blocks(int W, int lane_probes) { return W <= 2 ? (lane_probes >= 4 ? 6 : 8) : 5; }
+constexpr int probe_min_blocks(int W, int lane_probes) {
+  return W <= 2 ? (lane_probes >= 4 ? 6 : W == 2 ? MIHG_MINB_W2 : 8) : 5;
+}
 #endif
 template <int W, bool kTrace, int kLaneProbes>
 __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes)) mih_probe_kernel(ProbeArgs p) {

@@ -245,6 +245,56 @@ def test_random_shapes_vs_oracle(cuda_ok, port, bits, m, n):
             assert np.array_equal(t[:, 4], od[:, -1]), "final_radius == d_k"
             assert np.array_equal(t, closed_form_traces(db.raw_words(), bits, m, qs, t[:, 4])), (layout, k)
 
+@pytest.mark.parametrize("comps,n", [(64, 1_000_000), (2, 400_000)])
+def test_clustered_codes_on_32bit_sparse_tables(cuda_ok, port, comps, n):
+    # Config 4's shape at test size: Gaussian-mixture codes (csrc/gen.cu restated by the oracle),
+    # m = 2 tables of 32 bits (sparse directory, residual table-order codes). Few components give
+    # saturated directory groups (escape records), buckets above the inline limit (piece queue)
+    # and buffers that fill while U is loose (compaction kernel). ids/dists against the oracle's
+    # exhaustive scan; traces against the closed forms (index.hpp:185-253 semantics).
+    mg = _mg()
+    codes = port.gen_mixture(0, n, 64, 128, comps, 0x4C0FFEE, 0x51)
+    qs = port.gen_mixture(0, 24, 64, 128, comps, 0x4C0FFEE, 0x52)
+    if comps == 2:
+        # two crowded buckets: 3000 codes sharing one table-0 key and 2000 sharing one table-1 key,
+        # the other half a few flips away from the seed code; the seeds join the queries
+        rng = np.random.default_rng(5)
+        c0, c1 = codes[10, 0], codes[20, 0]
+        flips = lambda cnt: np.bitwise_or.reduce(np.uint64(1) << rng.integers(0, 32, (cnt, 3)).astype(np.uint64), axis=1)
+        codes[100:3100, 0] = (c0 & np.uint64(0xFFFFFFFF)) | (((c0 >> np.uint64(32)) ^ flips(3000)) << np.uint64(32))
+        codes[5000:7000, 0] = (c1 & np.uint64(0xFFFFFFFF00000000)) | ((c1 & np.uint64(0xFFFFFFFF)) ^ flips(2000))
+        qs[0, 0], qs[1, 0] = c0, c1
+    idx = mg.MihIndex.build(mg.CodeDatabase(64, codes), mg.consecutive_partition(64, 2))
+    tabs = [idx.table(j) for j in range(2)]
+    assert all(not t.dense() for t in tabs)
+    if comps == 2:  # the paths this case is here for
+        assert max(t.max_bucket_size() for t in tabs) > 128
+        assert sum(int(t._info.escaped_blocks) for t in tabs) > 0
+    for k in (1, 100, 1000):
+        ids, dists, tr = idx.knn_search_batch(qs, k, with_trace=True)
+        oi, od = port.scan_knn(codes, 64, qs, k)
+        assert np.array_equal(dists, od), k
+        assert np.array_equal(ids, oi), k
+        ui, ud = idx.knn_search_batch(qs, k)  # untraced product path
+        assert np.array_equal(ui, oi) and np.array_equal(ud, od), k
+        t = _trace_array(tr)
+        assert np.array_equal(t[:, 4], od[:, -1]), "final_radius == d_k"
+        assert np.array_equal(t, closed_form_traces(codes, 64, 2, qs, t[:, 4])), k
+    if comps == 2:
+        # small candidate buffers: the crowded buckets overflow them while U is loose, so the
+        # compaction kernel and the exact re-run pass both run
+        import os
+
+        os.environ["MIHG_BUFFER_CAP"] = "2200"
+        try:
+            for k in (100, 1000):
+                oi, od = port.scan_knn(codes, 64, qs, k)
+                ids, dists, tr = idx.knn_search_batch(qs, k, with_trace=True)
+                assert np.array_equal(ids, oi) and np.array_equal(dists, od), k
+                assert np.array_equal(_trace_array(tr), closed_form_traces(codes, 64, 2, qs, od[:, -1])), k
+        finally:
+            del os.environ["MIHG_BUFFER_CAP"]
+
 
 @pytest.mark.parametrize("layout", ["auto", "sparse"])
 def test_table_stats_match_reference(cuda_ok, golden, layout):

@@ -31,3 +31,18 @@ def test_knn_device_orders_with_caller_stream(cuda_ok, port):
     oi, od = port.scan_knn(db.raw_words(), 64, qs, k)
     assert np.array_equal(got_i.cpu().numpy().view(np.uint32), oi)
     assert np.array_equal(got_d.cpu().numpy().view(np.uint32), od)
+
+
+def test_calibrate_random_lookups(cuda_ok):
+    """The calibration entry point (bench.py's random-access reference) returns a positive rate and
+    rejects bad arguments."""
+    import ctypes as C
+
+    from paper_1307_2982_b200 import _lib
+
+    L = _lib.lib()
+    rate = C.c_double(0.0)
+    _lib.check(L.mihg_calibrate_random_lookups(0, 8 << 20, 16 << 20, 29, C.byref(rate)))
+    assert rate.value > 1e8
+    assert L.mihg_calibrate_random_lookups(0, 8, 16 << 20, 29, C.byref(rate)) != 0
+    assert L.mihg_calibrate_random_lookups(0, 8 << 20, 16 << 20, 101, C.byref(rate)) != 0

@@ -4,7 +4,7 @@
 set -u
 TAG=$1; C=${2:-4}; OUT=gpurun_out
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct,smsp__inst_executed.sum,lts__t_sectors_op_read.sum,smsp__issue_active.avg.pct_of_peak_sustained_active \
-    --clock-control none -k regex:"mih_probe_kernel|mih_piece_kernel|mih_group" --csv --log-file $OUT/${TAG}_rounds.csv \
+    --clock-control none -k regex:"mih_probe_kernel|mih_piece_kernel" --csv --log-file $OUT/${TAG}_rounds.csv \
     python tools/one_step.py --config $C > /dev/null 2>&1
 python - "$OUT/${TAG}_rounds.csv" > $OUT/${TAG}_rounds.txt <<'PY'
 import csv, sys
@@ -15,7 +15,7 @@ per = {}
 for r in rows[h + 1:]:
     if len(r) < len(H): continue
     name, unit, val = r[H.index('Metric Name')], r[H.index('Metric Unit')], float(r[H.index('Metric Value')].replace(',', ''))
-    scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'nsecond': 1e-6, 'usecond': 1e-3, 'msecond': 1, 'second': 1e3}.get(unit, 1)
+    scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'nsecond': 1e-6, 'usecond': 1e-3, 'msecond': 1, 'second': 1e3, 'ns': 1e-6, 'us': 1e-3, 'ms': 1, 's': 1e3}.get(unit, 1)
     d = per.setdefault(int(r[H.index('ID')]), {'k': r[H.index('Kernel Name')][:40]})
     d[name] = val * scale
 tot = {}

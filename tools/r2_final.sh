@@ -28,6 +28,8 @@ head -8 $O/launches_bench_c4_summary.csv
 timeout 1500 bash tools/ncu_top.sh ${1:-r2final}/c4_probe mih_probe_kernel python tools/one_step.py --config 4
 python tools/ncu_summary.py $O/c4_probe.ncu-rep > $O/ncu_full_c4_probe.txt 2>&1
 python tools/ncu_mem_sites.py $O/c4_probe.ncu-rep 25 > $O/ncu_mem_sites_c4_probe.txt 2>&1
-timeout 900 bash tools/ncu_top.sh ${1:-r2final}/k7_256 tc_scan_kernel python tools/bench_tcscan.py 2e7 256 10000 100 tc
+python tools/ncu_src_lines.py $O/c4_probe.ncu-rep 40 > $O/ncu_src_lines_c4_probe.txt 2>&1
+timeout 900 bash tools/ncu_rounds.sh ${1:-r2final}/c4 4 > /dev/null 2>&1
+timeout 900 bash tools/ncu_top.sh ${1:-r2final}/k7_256 tc_scan_kernel python tools/bench_tcscan.py 4e8 256 10000 100 tc
 python tools/ncu_summary.py $O/k7_256.ncu-rep > $O/ncu_full_k7_256.txt 2>&1
 for c in 4 3 2; do timeout 1200 bash tools/ncu_traffic.sh $c > $O/traffic_c$c.json 2>&1; mv gpurun_out/traffic_c$c.* $O/ 2>/dev/null; tail -1 $O/traffic_c$c.json; done

@@ -1211,6 +1211,7 @@ RerunResult rerun_pass(Index& idx, const ProbeArgs& p, const uint32_t* d_rerun, 
   MIHG_CUDA(cudaMemsetAsync(ws.bufcnt.get(), 0, nq * 4, st));
   ProbeArgs rp = p;
   rp.d_nact = nullptr;  // host-planned: the re-run list size is known
+  rp.pieces = ws.pieces.get();
   rp.hist = nullptr;
   rp.trc = nullptr;
   rp.ubound = ws.final_r.get();
@@ -1300,7 +1301,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   uint32_t* act_buf[2] = {ws.act0.get(), ws.act1.get()};
   uint64_t nact_known = nq;
   uint32_t r_known = 0;  // nact_known == nact entering round r_known
-  uint64_t acc = 0;
+  uint64_t acc = 0, cand_bound = 0;
   const double alpha = (d_tr || (part && part->id_shards) || !hybrid_ok) ? 0.0 : hybrid_alpha();
   const double scan_pairs = double(idx.n) * scan_cost_per_code(idx.bits),
                probe_pairs = 36.0 + 15.0 * (idx.W - 1);
@@ -1359,8 +1360,13 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
     }
     acc += ring;
     lookups_prefix.push_back(acc);
+    // no query can hold more keys than ring x (largest bucket) per round: below the inline limit
+    // the round has no piece queue, and below half a buffer no compaction (launch-bound batches)
+    const uint64_t maxb = idx.tables[a]->max_bucket;
+    cand_bound = std::min<uint64_t>(cand_bound + ring * maxb, uint64_t(1) << 62);
     if (ring) {
       p.tab = idx.tables[a]->view();
+      p.pieces = maxb > (p.tab.dense ? p.inline_max : p.inline_max_sparse) ? ws.pieces.get() : nullptr;
       p.a = a;
       p.rr = rr;
       p.r = r;
@@ -1391,9 +1397,11 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
                                              ws.final_r.get(), ws.bufcnt.get(), cap, ws.compact_list.get(),
                                              ws.compact_n.get() + r);
     MIHG_LAUNCH();
-    mih_compact_kernel<<<unsigned(std::min<uint64_t>(nact_known, uint64_t(device_sm_count()) * 2)), 1024, 0, st>>>(
-        ws.compact_list.get(), ws.compact_n.get() + r, ws.bufcnt.get(), ws.buf.get(), cap);
-    MIHG_LAUNCH();
+    if (cand_bound > cap / 2) {
+      mih_compact_kernel<<<unsigned(std::min<uint64_t>(nact_known, uint64_t(device_sm_count()) * 2)), 1024, 0, st>>>(
+          ws.compact_list.get(), ws.compact_n.get() + r, ws.bufcnt.get(), ws.buf.get(), cap);
+      MIHG_LAUNCH();
+    }
     MIHG_CUDA(cudaMemcpyAsync(ws.h_nact + r + 1, ws.nact_dev.get() + r + 1, 4, cudaMemcpyDeviceToHost, st));
     MIHG_CUDA(cudaEventRecord(ws.ev_round[r], st));
     // keep at most kRunAhead rounds unread; read any that already finished. Partitioned calls read

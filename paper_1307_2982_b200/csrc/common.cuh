@@ -78,6 +78,8 @@ struct DevTable {
   // the other substring in the code word (0 or 32). rcodes != nullptr replaces `codes`.
   const uint32_t* rcodes;
   uint32_t rshift;
+  // bounds for the assert build (make EXTRA=-DMIHG_DEBUG): entries in the table, escape records
+  uint32_t n_entries, n_esc;
 };
 
 // Substring j of the partition: contiguous run (offset, len) or explicit positions.
@@ -106,6 +108,7 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
 // the same key slice: keep it in L2 (evict last); the candidate codes behind it stream through
 // (evict first, verify_residual).
 __device__ __forceinline__ uint4 load_dir_group(const DevTable& t, uint32_t gi) {
+  MIHG_DASSERT(t.dir && t.s >= kDirBucketsLog2 && uint64_t(gi) < (uint64_t(1) << (t.s - kDirBucketsLog2)));
   uint4 g;
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -127,21 +130,26 @@ __device__ __forceinline__ void decode_dir_group(const DevTable& t, const uint4&
   // Escaped group (some bucket saturated at count 7): `base` holds the escape record's index, so
   // every non-empty bucket of the group reads its exact start from the record.
   if (g.x & g.y & g.z) {
+    MIHG_DASSERT(g.w < t.n_esc);
     const uint32_t* e = t.esc + uint64_t(g.w) * kEscStarts + tt;
     lo = __ldg(e);
     hi = __ldg(e + 1);
+    MIHG_DASSERT(lo < hi && hi <= t.n_entries);
     return;
   }
   lo = g.w + __popc(g.x & below) + 2u * __popc(g.y & below) + 4u * __popc(g.z & below);
   hi = lo + c;
+  MIHG_DASSERT(hi <= t.n_entries);
 }
 
 // ---- bucket probe: [lo, hi) slice of ids[] for bucket `v` (table.hpp:178-188 semantics).
 __device__ __forceinline__ void probe_bucket(const DevTable& t, uint32_t v, uint32_t& lo,
                                              uint32_t& hi) {
   if (t.dense) {
+    MIHG_DASSERT(uint64_t(v) < (uint64_t(1) << t.s));
     lo = __ldg(t.offsets + v);
     hi = __ldg(t.offsets + v + 1);
+    MIHG_DASSERT(lo <= hi && hi <= t.n_entries);
     return;
   }
   if (t.occ && !((__ldg(t.occ + (v >> 5)) >> (v & 31)) & 1u)) {  // empty: an L2 hit, no sector

@@ -27,7 +27,7 @@ struct TableStorage {
   uint64_t max_bucket = 0;
   DevTable view() const {
     return DevTable{ids.get(), offsets.get(), dir.get(), esc.get(), tcodes.get(), occ.get(), s,
-                    dense ? 1u : 0u, rcodes.get(), rshift};
+                    dense ? 1u : 0u, rcodes.get(), rshift, uint32_t(ids.size()), uint32_t(escaped_blocks)};
   }
   // frees every device buffer (stream-ordered on the index stream, before that stream goes away)
   void release() {

@@ -200,6 +200,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 
 struct ProbeArgs {
   const uint64_t* codes;
+  uint64_t n_codes;        // codes in the index (assert build)
   const uint64_t* qcodes;  // nq * nw
   const uint32_t* qsub;    // nq * m
   DevTable tab;
@@ -388,6 +389,7 @@ template <bool kTrace>
 __device__ __forceinline__ void verify_residual(const ProbeArgs& p, const QueryCtx& c, bool v0, uint32_t e0,
                                                 bool v1, uint32_t e1, uint64_t q, uint64_t& n_new) {
   const uint32_t qo = uint32_t(q >> p.tab.rshift);
+  MIHG_DASSERT((!v0 || e0 < p.tab.n_entries) && (!v1 || e1 < p.tab.n_entries));
   uint32_t r0 = 0, r1 = 0;  // candidate codes stream through L2: evict first
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -429,12 +431,14 @@ __device__ __forceinline__ void verify_entries(const ProbeArgs& p, const QueryCt
   }
   Diff<W> d0, d1;
   uint32_t id0 = 0, id1 = 0;
+  MIHG_DASSERT((!v0 || e0 < p.tab.n_entries) && (!v1 || e1 < p.tab.n_entries));
   if (p.tab.codes) {
     if (v0) d0.load(p.tab.codes, e0, qc, nw);
     if (v1) d1.load(p.tab.codes, e1, qc, nw);
   } else {
     if (v0) id0 = __ldg(p.tab.ids + e0);
     if (v1) id1 = __ldg(p.tab.ids + e1);
+    MIHG_DASSERT((!v0 || id0 < p.n_codes) && (!v1 || id1 < p.n_codes));
     if (v0) d0.load(p.codes, id0, qc, nw);
     if (v1) d1.load(p.codes, id1, qc, nw);
   }
@@ -463,6 +467,7 @@ __device__ __forceinline__ void keep_entries(const ProbeArgs& p, const QueryCtx&
                                              uint32_t b0, uint32_t b1) {
   const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
   const uint32_t n0 = __popc(b0), total = n0 + __popc(b1);
+  MIHG_DASSERT((!k0 || (dist0 < p.b1 && id0 < p.n_codes)) && (!k1 || (dist1 < p.b1 && id1 < p.n_codes)));
   uint32_t base = 0;
   if (lane == 0) base = atomicAdd(p.bufcnt + c.q, total);
   base = __shfl_sync(~0u, base, 0);
@@ -656,6 +661,7 @@ __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes
 #pragma unroll
       for (int b = 0; b < kLaneProbes; ++b) {
         if (cnt[b]) {
+          MIHG_DASSERT(sp < uint32_t(kWarpBuckets));
           s_lo[wib][sp] = lo[b];
           s_off[wib][sp] = off;
           ++sp;
@@ -678,6 +684,7 @@ __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes
         mhi = __reduce_or_sync(~0u, mhi);
         const uint32_t nlo = __popc(mlo);
         const uint32_t a0 = cur + __popc(mlo & le) - 1, a1 = cur + nlo + __popc(mhi & le) - 1;
+        MIHG_DASSERT(a0 < n_ne && a1 < n_ne && s_off[wib][a0] <= t0 + lane && s_off[wib][a1] <= t0 + 32 + lane);
         uint32_t e[2];
         bool v[2];
         v[0] = t0 + lane < total;
@@ -1137,6 +1144,7 @@ double uniform_model_lookups(const Index& idx, uint32_t k) {
 ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   ProbeArgs p{};
   p.codes = idx.codes.get();
+  p.n_codes = idx.n;
   p.qcodes = d_q;
   p.qsub = ws.qsub.get();
   p.subs = idx.d_subs.get();

@@ -38,7 +38,7 @@ def main():
                 bad += not (np.array_equal(si, wi) and np.array_equal(sd, wd))
         os.environ.pop("MIHG_SCAN_KERNEL", None)
         os.environ.pop("MIHG_TC_PAIR", None)
-        offs, ri, rd = idx.range_search_batch(qs[:5], bits // 8)
+        offs, ri, rd, _ = idx.range_search_batch(qs[:5], bits // 8)
         bad += int(offs[-1] != len(ri))
     # heavy ties: large segments through the radix selection path and the re-run pass
     centres = mg.gen_uniform(3, 64, 99).raw_words()

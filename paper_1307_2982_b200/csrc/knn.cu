@@ -18,7 +18,7 @@
 //    every round from the exact histogram) are histogrammed and appended to a bounded per-query
 //    buffer; a per-query drop-minimum records whether anything relevant overflowed.
 //  * mih_round_end_kernel: termination test sum_{d<=r} hist >= k (index.hpp:209, :232), U update,
-//    buffer compaction, next active list.
+//    next active list, and the list of buffers mih_compact_kernel trims to the new bound.
 //  * selection: exact top-k of the buffered keys (dist << 32 | id) — select.cu. Queries whose
 //    buffer overflowed with a relevant key re-run their steps with the final radius as the bound
 //    into exactly-sized buffers.
@@ -497,23 +497,19 @@ constexpr int kProbeWarps = kProbeThreads / 32;
 
 // Warp-cooperative MIH step. A work unit is (active query, warp chunk of 32*chunk ring indices);
 // lane l walks its own `chunk` consecutive ring indices, kLaneProbes per iteration (independent
-// directory loads in flight). The warp prefix-sums the 128 bucket sizes and verifies the union
-// of the entries lane-parallel, two per lane per pass (entry t belongs to the bucket whose
-// [off, off + cnt) holds t: 7-step binary search in shared memory), so bucket-size skew never
-// idles the warp. Buckets above kInlineMax go to the piece queue.
+// directory loads in flight). The warp prefix-sums the bucket sizes and verifies the union of the
+// entries lane-parallel, two per lane per pass (entry t belongs to the bucket whose
+// [off, off + cnt) holds t: a popcount rank over the window's bucket starts), so bucket-size skew
+// never idles the warp. Buckets above the inline limit go to the piece queue.
 // Resident blocks per SM (MIHG_PROBE_MINB overrides the W <= 2 value): 8 (32 registers) for
 // 1-2 probes per lane, 6 (40 registers, spills 172 -> 40 B) for the 4-probe sparse variant.
 // Measured B200 sweep: config 4 (4 probes) 8/6/5/4 blocks = 951K/970K/872K/852K q/s; config 3
 // (2 probes) 271K/242K/227K/194K — occupancy wins over spills except for the 4-probe kernel.
-#ifndef MIHG_MINB_W2
-#define MIHG_MINB_W2 8
-#endif
+// (W = 2 at 6 blocks: config 2 895K -> 879K.)
 #ifdef MIHG_PROBE_MINB
 constexpr int probe_min_blocks(int W, int) { return W <= 2 ? MIHG_PROBE_MINB : 5; }
 #else
-constexpr int probe_min_blocks(int W, int lane_probes) {
-  return W <= 2 ? (lane_probes >= 4 ? 6 : W == 2 ? MIHG_MINB_W2 : 8) : 5;
-}
+constexpr int probe_min_blocks(int W, int lane_probes) { return W <= 2 ? (lane_probes >= 4 ? 6 : 8) : 5; }
 #endif
 template <int W, bool kTrace, int kLaneProbes>
 __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes)) mih_probe_kernel(ProbeArgs p) {
@@ -754,7 +750,7 @@ __global__ void mih_init_kernel(uint64_t nq, uint32_t bits, uint32_t* ubound, ui
   }
 }
 
-// One warp per active query: termination test, bound update, buffer compaction.
+// One warp per active query: termination test, bound update, compaction list.
 __global__ void mih_round_end_kernel(const uint32_t* __restrict__ act_in, uint32_t nact,
                                      const uint32_t* __restrict__ d_nact_in,
                                      uint32_t* __restrict__ act_out, uint32_t* __restrict__ nact_out,

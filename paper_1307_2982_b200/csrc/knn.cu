@@ -903,8 +903,10 @@ void launch_probe(const ProbeArgs& p, cudaStream_t st) {
   const int lp = lane_probes(p.tab);
   const int minb = lp == 1 ? probe_min_blocks(W, 1) : lp == 4 ? probe_min_blocks(W, 4) : probe_min_blocks(W, 2);
   const uint64_t max_blocks = uint64_t(device_sm_count()) * minb;  // one resident wave
-  const unsigned grid = p.slice_bits || p.d_nact ? unsigned(max_blocks)
-                                                : unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
+  // unsliced rounds: the host's plan (made with an upper bound of the active count) sizes the
+  // grid — small rounds launch few blocks; the unit loop strides, so any grid is correct
+  const unsigned grid = p.slice_bits ? unsigned(max_blocks)
+                                     : unsigned(std::max<uint64_t>(1, std::min(blocks_needed, max_blocks)));
   if (p.pieces) MIHG_CUDA(cudaMemsetAsync(p.piece_count, 0, 4, st));
   switch (lp) {
     case 1: mih_probe_kernel<W, kTrace, 1><<<grid, kProbeThreads, 0, st>>>(p); break;

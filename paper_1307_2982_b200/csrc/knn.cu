@@ -203,6 +203,7 @@ struct ProbeArgs {
   uint64_t n_codes;        // codes in the index (assert build)
   const uint64_t* qcodes;  // nq * nw
   const uint32_t* qsub;    // nq * m
+  const DevTable* tables;  // the index's m tables on the device (mih_solo_kernel switches per step)
   DevTable tab;
   const DevSubstring* subs;
   const uint64_t* submask;
@@ -495,6 +496,153 @@ __device__ __forceinline__ void keep_entries(const ProbeArgs& p, const QueryCtx&
 constexpr int kProbeThreads = 256;
 constexpr int kProbeWarps = kProbeThreads / 32;
 
+// One warp unit of an MIH step: query q, ring indices [part * 32 * pchunk, ... + 32 * pchunk) of a
+// (sub-)ring of `ring` indices with zbits flips among the low sbits key bits (`high` = the fixed
+// top flip pattern of a sliced round). s_lo / s_off: the warp's bucket list in shared memory.
+template <int W, bool kTrace, int kLaneProbes>
+__device__ __forceinline__ void probe_unit(const ProbeArgs& p, uint32_t q, uint32_t part, uint32_t pchunk,
+                                           uint32_t ring, uint32_t high, uint32_t zbits, uint32_t sbits,
+                                           uint32_t (*s_lo)[32 * kLaneProbes], uint32_t (*s_off)[32 * kLaneProbes]) {
+  constexpr int kNzBits = kLaneProbes == 1 ? 1 : kLaneProbes == 2 ? 2 : kLaneProbes == 4 ? 3 : 4;
+  const uint32_t nw = W ? W : p.nw;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, lt = lanemask_lt();
+  const uint32_t span = pchunk * 32;
+  const uint32_t ubeg = part * span;
+  const uint32_t uend = uint32_t(min(uint64_t(ring), uint64_t(ubeg) + span));
+  uint32_t i = ubeg + lane * pchunk;
+  const uint32_t iend = min(uend, i + pchunk);
+  uint32_t mask = i < iend ? unrank_comb(p.binom, i, sbits, zbits) : 0u;
+  const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
+  uint64_t qreg[W ? W : 1];
+  const uint64_t* qptr = p.qcodes + uint64_t(q) * nw;
+  if constexpr (W > 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) qreg[w] = __ldg(qptr + w);
+  }
+  const uint64_t* qc = W ? qreg : qptr;
+  const QueryCtx ctx = query_ctx(p, q);
+  uint64_t n_cand = 0, n_new = 0;
+  for (uint32_t it = 0; it < pchunk; it += kLaneProbes) {
+    uint32_t lo[kLaneProbes], cnt[kLaneProbes];
+#pragma unroll
+    for (int b = 0; b < kLaneProbes; ++b) {
+      uint32_t l = 0, h = 0;
+      if (i < iend && it + b < pchunk) {
+        const uint32_t v = qa ^ (high | mask);
+        if (p.part_bits == 0 || (v >> (p.tab.s - p.part_bits)) == p.part_id) probe_bucket(p.tab, v, l, h);
+        mask = next_comb(mask);
+        ++i;
+      }
+      lo[b] = l;
+      cnt[b] = h - l;
+    }
+    if (p.prefetch && !p.tab.dense) {
+      // the next iteration's directory sectors start their DRAM trip now, overlapping this
+      // iteration's verification (no registers held: a cache prefetch)
+      uint32_t mk = mask, ii = i;
+#pragma unroll
+      for (int b = 0; b < kLaneProbes; ++b) {
+        if (ii < iend && it + kLaneProbes + b < pchunk) {
+          const DirGroup* blk = p.tab.dir + ((qa ^ (high | mk)) >> kDirBucketsLog2);
+          if (p.prefetch == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(blk));
+          else asm volatile("prefetch.global.L2 [%0];" ::"l"(blk));
+          mk = next_comb(mk);
+          ++ii;
+        }
+      }
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int b = 0; b < kLaneProbes; ++b) {
+      n_cand += cnt[b];
+      if (cnt[b] > (p.tab.dense ? p.inline_max : p.inline_max_sparse) && p.pieces) {
+        const uint32_t np = (cnt[b] + p.piece_size - 1) / p.piece_size;
+        const uint32_t at = atomicAdd(p.piece_count, np);
+        if (at + np <= p.piece_cap) {
+          for (uint32_t t = 0; t < np; ++t)
+            p.pieces[at + t] = Piece{q, lo[b] + t * p.piece_size, min(p.piece_size, cnt[b] - t * p.piece_size), 0};
+          cnt[b] = 0;
+        } else {
+          for (uint32_t t = at; t < p.piece_cap && t < at + np; ++t) p.pieces[t] = Piece{q, 0, 0, 0};
+        }
+      }
+      mine += cnt[b];
+    }
+    // warp exclusive prefix of the per-lane totals; buckets laid out lane-major
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(~0u, incl, o);
+      if (lane >= uint32_t(o)) incl += y;
+    }
+    const uint32_t total = __shfl_sync(~0u, incl, 31);
+    if (total == 0) continue;
+#ifdef MIHG_TC_DEBUG
+    if (p.debug_probe_only) continue;  // traffic attribution: directory probes alone
+#endif
+    // the non-empty buckets, compacted in lane-major order: (first entry, offset in the union)
+    uint32_t nz = 0;
+#pragma unroll
+    for (int b = 0; b < kLaneProbes; ++b) nz += cnt[b] != 0;
+    uint32_t sp = 0, n_ne = 0;
+#pragma unroll
+    for (int bit = 0; bit < kNzBits; ++bit) {
+      const uint32_t bal = __ballot_sync(~0u, (nz >> bit) & 1u);
+      sp += __popc(bal & lt) << bit;
+      n_ne += __popc(bal) << bit;
+    }
+    uint32_t off = incl - mine;
+#pragma unroll
+    for (int b = 0; b < kLaneProbes; ++b) {
+      if (cnt[b]) {
+        MIHG_DASSERT(sp < uint32_t(32 * kLaneProbes));
+        s_lo[wib][sp] = lo[b];
+        s_off[wib][sp] = off;
+        ++sp;
+        off += cnt[b];
+      }
+    }
+    __syncwarp();
+    // Entry t of the union belongs to the last bucket whose offset is <= t. Offsets are distinct
+    // and ascending, so the buckets starting inside a 64-entry window are the next <= 64 list
+    // slots after `cur` (the count of buckets that started before the window): their start
+    // positions, OR-reduced into a 64-bit mask, rank every entry with one popcount.
+    uint32_t cur = 0;
+    const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
+    for (uint32_t t0 = 0; t0 < total; t0 += 64) {
+      const uint32_t i0 = cur + lane, i1 = i0 + 32;
+      const uint32_t o0 = i0 < n_ne ? s_off[wib][i0] - t0 : 64u, o1 = i1 < n_ne ? s_off[wib][i1] - t0 : 64u;
+      uint32_t mlo = (o0 < 32 ? 1u << o0 : 0u) | (o1 < 32 ? 1u << o1 : 0u);
+      uint32_t mhi = (o0 - 32 < 32 ? 1u << (o0 - 32) : 0u) | (o1 - 32 < 32 ? 1u << (o1 - 32) : 0u);
+      mlo = __reduce_or_sync(~0u, mlo);
+      mhi = __reduce_or_sync(~0u, mhi);
+      const uint32_t nlo = __popc(mlo);
+      const uint32_t a0 = cur + __popc(mlo & le) - 1, a1 = cur + nlo + __popc(mhi & le) - 1;
+      MIHG_DASSERT(a0 < n_ne && a1 < n_ne && s_off[wib][a0] <= t0 + lane && s_off[wib][a1] <= t0 + 32 + lane);
+      uint32_t e[2];
+      bool v[2];
+      v[0] = t0 + lane < total;
+      v[1] = t0 + 32 + lane < total;
+      e[0] = s_lo[wib][a0] + (t0 + lane - s_off[wib][a0]);
+      e[1] = s_lo[wib][a1] + (t0 + 32 + lane - s_off[wib][a1]);
+      cur += nlo + __popc(mhi);
+      verify_entries<W, kTrace>(p, ctx, v[0], e[0], v[1], e[1], qc, nw, n_new);
+    }
+    __syncwarp();
+  }
+  if (kTrace) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      n_cand += __shfl_xor_sync(~0u, n_cand, o);
+      n_new += __shfl_xor_sync(~0u, n_new, o);
+    }
+    if (lane == 0 && n_cand) {
+      atomicAdd(p.trc + 2 * uint64_t(q), (unsigned long long)n_cand);
+      if (n_new) atomicAdd(p.trc + 2 * uint64_t(q) + 1, (unsigned long long)n_new);
+    }
+  }
+}
+
 // Warp-cooperative MIH step. A work unit is (active query, warp chunk of 32*chunk ring indices);
 // lane l walks its own `chunk` consecutive ring indices, kLaneProbes per iteration (independent
 // directory loads in flight). The warp prefix-sums the bucket sizes and verifies the union of the
@@ -514,11 +662,9 @@ constexpr int probe_min_blocks(int W, int lane_probes) { return W <= 2 ? (lane_p
 template <int W, bool kTrace, int kLaneProbes>
 __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes)) mih_probe_kernel(ProbeArgs p) {
   constexpr int kWarpBuckets = 32 * kLaneProbes;
-  constexpr int kNzBits = kLaneProbes == 1 ? 1 : kLaneProbes == 2 ? 2 : kLaneProbes == 4 ? 3 : 4;
   __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
   __shared__ uint32_t s_off[kProbeWarps][kWarpBuckets];
-  const uint32_t nw = W ? W : p.nw;
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, lt = lanemask_lt();
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint32_t pchunk = p.chunk;
   uint64_t pcpq = p.cpq, ptotal = p.total;
   if (p.d_nact) {  // device-planned round
@@ -569,139 +715,91 @@ __global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes
     }
     const uint32_t q = p.active[slot];
     if (p.rlimit && p.r > p.rlimit[q]) continue;
-    const uint32_t ubeg = part * span;
-    const uint32_t uend = uint32_t(min(uint64_t(ring), uint64_t(ubeg) + span));
-    uint32_t i = ubeg + lane * pchunk;
-    const uint32_t iend = min(uend, i + pchunk);
-    uint32_t mask = i < iend ? unrank_comb(p.binom, i, sbits, zbits) : 0u;
-    const uint32_t qa = p.qsub[uint64_t(q) * p.m + p.a];
-    uint64_t qreg[W ? W : 1];
-    const uint64_t* qptr = p.qcodes + uint64_t(q) * nw;
-    if constexpr (W > 0) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) qreg[w] = __ldg(qptr + w);
-    }
-    const uint64_t* qc = W ? qreg : qptr;
-    const QueryCtx ctx = query_ctx(p, q);
-    uint64_t n_cand = 0, n_new = 0;
-    for (uint32_t it = 0; it < pchunk; it += kLaneProbes) {
-      uint32_t lo[kLaneProbes], cnt[kLaneProbes];
-#pragma unroll
-      for (int b = 0; b < kLaneProbes; ++b) {
-        uint32_t l = 0, h = 0;
-        if (i < iend && it + b < pchunk) {
-          const uint32_t v = qa ^ (high | mask);
-          if (p.part_bits == 0 || (v >> (p.tab.s - p.part_bits)) == p.part_id) probe_bucket(p.tab, v, l, h);
-          mask = next_comb(mask);
-          ++i;
-        }
-        lo[b] = l;
-        cnt[b] = h - l;
+    probe_unit<W, kTrace, kLaneProbes>(p, q, part, pchunk, ring, high, zbits, sbits, s_lo, s_off);
+  }
+}
+
+// Small batches: ONE block per query runs the query's whole radius loop (index.hpp:208-234) —
+// step r probes ring r / m of table r mod m with the block's warps (probe_unit), a block barrier
+// replaces the per-round kernel launches, warp 0 applies the stopping rule and tightens the
+// bound. With a few hundred lookups per round the round-synchronous path is bound by launch and
+// dependent-load latency per round (config 1: 13 rounds x ~70 us); here a query's rounds cost a
+// block barrier each and different queries do not wait for one another. The step's ProbeArgs
+// live in shared memory (table, a, rr, r change per step).
+template <int W, bool kTrace, int kLaneProbes>
+__global__ void __launch_bounds__(kProbeThreads, probe_min_blocks(W, kLaneProbes))
+    mih_solo_kernel(ProbeArgs p0, uint32_t nq, uint32_t k, uint32_t bits, uint32_t* __restrict__ ubound,
+                    uint32_t* __restrict__ final_r) {
+  constexpr int kWarpBuckets = 32 * kLaneProbes;
+  __shared__ uint32_t s_lo[kProbeWarps][kWarpBuckets];
+  __shared__ uint32_t s_off[kProbeWarps][kWarpBuckets];
+  constexpr uint32_t kSoloTables = 16;  // tables kept in shared memory (more: read per step)
+  __shared__ ProbeArgs sp;
+  __shared__ DevTable s_tab[kSoloTables];
+  __shared__ uint32_t s_done;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (threadIdx.x < min(p0.m, kSoloTables)) s_tab[threadIdx.x] = p0.tables[threadIdx.x];
+  for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) sp = p0;
+    for (uint32_t r = 0; r <= bits; ++r) {
+      const uint32_t a = r % p0.m, rr = r / p0.m;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        sp.tab = a < kSoloTables ? s_tab[a] : p0.tables[a];
+        sp.a = a;
+        sp.rr = rr;
+        sp.r = r;
       }
-      if (p.prefetch && !p.tab.dense) {
-        // the next iteration's directory sectors start their DRAM trip now, overlapping this
-        // iteration's verification (no registers held: a cache prefetch)
-        uint32_t mk = mask, ii = i;
+      __syncthreads();
+      const uint32_t s = sp.tab.s;
+      const uint32_t ring = rr <= s ? uint32_t(__ldg(p0.binom + s * kBinomStride + rr)) : 0u;
+      if (ring) {
+        const uint32_t want = (ring + 32 * kProbeWarps - 1) / (32 * kProbeWarps);  // one unit per warp
+        const uint32_t pchunk = min(max(want, 1u), 256u);
+        const uint32_t cpq = (ring + 32 * pchunk - 1) / (32 * pchunk);
+        for (uint32_t part = wib; part < cpq; part += kProbeWarps)
+          probe_unit<W, kTrace, kLaneProbes>(sp, q, part, pchunk, ring, 0u, rr, s, s_lo, s_off);
+      }
+      __threadfence();
+      __syncthreads();
+      if (wib == 0) {  // the stopping rule and the bound, as mih_round_end_kernel (L2 reads: the
+                       // histogram is updated by atomics, which bypass L1)
+        const uint32_t U = __ldcg(ubound + q);
+        const uint32_t* h = p0.hist + uint64_t(q) * p0.b1;
+        uint32_t run = 0, settled = 0, newU = U;
+        bool found = false;
+        for (uint32_t d0 = 0; d0 <= U; d0 += 32) {
+          const uint32_t d = d0 + lane;
+          uint32_t v = d <= U ? __ldcg(h + d) : 0u;
 #pragma unroll
-        for (int b = 0; b < kLaneProbes; ++b) {
-          if (ii < iend && it + kLaneProbes + b < pchunk) {
-            const DirGroup* blk = p.tab.dir + ((qa ^ (high | mk)) >> kDirBucketsLog2);
-            if (p.prefetch == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(blk));
-            else asm volatile("prefetch.global.L2 [%0];" ::"l"(blk));
-            mk = next_comb(mk);
-            ++ii;
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(~0u, v, o);
+            if (lane >= uint32_t(o)) v += y;
           }
+          const uint32_t cum = run + v;
+          if (r >= d0 && r < d0 + 32) settled = __shfl_sync(~0u, cum, r - d0);
+          const uint32_t ok = __ballot_sync(~0u, d <= U && cum >= k);
+          if (!found && ok) {
+            newU = d0 + __ffs(ok) - 1;
+            found = true;
+          }
+          run = __shfl_sync(~0u, cum, 31);
         }
-      }
-      uint32_t mine = 0;
-#pragma unroll
-      for (int b = 0; b < kLaneProbes; ++b) {
-        n_cand += cnt[b];
-        if (cnt[b] > (p.tab.dense ? p.inline_max : p.inline_max_sparse) && p.pieces) {
-          const uint32_t np = (cnt[b] + p.piece_size - 1) / p.piece_size;
-          const uint32_t at = atomicAdd(p.piece_count, np);
-          if (at + np <= p.piece_cap) {
-            for (uint32_t t = 0; t < np; ++t)
-              p.pieces[at + t] = Piece{q, lo[b] + t * p.piece_size, min(p.piece_size, cnt[b] - t * p.piece_size), 0};
-            cnt[b] = 0;
+        if (r > U) settled = run;
+        if (lane == 0) {
+          if (settled >= k) {
+            final_r[q] = r;
+            s_done = 1;
           } else {
-            for (uint32_t t = at; t < p.piece_cap && t < at + np; ++t) p.pieces[t] = Piece{q, 0, 0, 0};
+            ubound[q] = newU;
+            s_done = 0;
           }
         }
-        mine += cnt[b];
       }
-      // warp exclusive prefix of the per-lane totals; buckets laid out lane-major
-      uint32_t incl = mine;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(~0u, incl, o);
-        if (lane >= uint32_t(o)) incl += y;
-      }
-      const uint32_t total = __shfl_sync(~0u, incl, 31);
-      if (total == 0) continue;
-#ifdef MIHG_TC_DEBUG
-      if (p.debug_probe_only) continue;  // traffic attribution: directory probes alone
-#endif
-      // the non-empty buckets, compacted in lane-major order: (first entry, offset in the union)
-      uint32_t nz = 0;
-#pragma unroll
-      for (int b = 0; b < kLaneProbes; ++b) nz += cnt[b] != 0;
-      uint32_t sp = 0, n_ne = 0;
-#pragma unroll
-      for (int bit = 0; bit < kNzBits; ++bit) {
-        const uint32_t bal = __ballot_sync(~0u, (nz >> bit) & 1u);
-        sp += __popc(bal & lt) << bit;
-        n_ne += __popc(bal) << bit;
-      }
-      uint32_t off = incl - mine;
-#pragma unroll
-      for (int b = 0; b < kLaneProbes; ++b) {
-        if (cnt[b]) {
-          MIHG_DASSERT(sp < uint32_t(kWarpBuckets));
-          s_lo[wib][sp] = lo[b];
-          s_off[wib][sp] = off;
-          ++sp;
-          off += cnt[b];
-        }
-      }
-      __syncwarp();
-      // Entry t of the union belongs to the last bucket whose offset is <= t. Offsets are distinct
-      // and ascending, so the buckets starting inside a 64-entry window are the next <= 64 list
-      // slots after `cur` (the count of buckets that started before the window): their start
-      // positions, OR-reduced into a 64-bit mask, rank every entry with one popcount.
-      uint32_t cur = 0;
-      const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
-      for (uint32_t t0 = 0; t0 < total; t0 += 64) {
-        const uint32_t i0 = cur + lane, i1 = i0 + 32;
-        const uint32_t o0 = i0 < n_ne ? s_off[wib][i0] - t0 : 64u, o1 = i1 < n_ne ? s_off[wib][i1] - t0 : 64u;
-        uint32_t mlo = (o0 < 32 ? 1u << o0 : 0u) | (o1 < 32 ? 1u << o1 : 0u);
-        uint32_t mhi = (o0 - 32 < 32 ? 1u << (o0 - 32) : 0u) | (o1 - 32 < 32 ? 1u << (o1 - 32) : 0u);
-        mlo = __reduce_or_sync(~0u, mlo);
-        mhi = __reduce_or_sync(~0u, mhi);
-        const uint32_t nlo = __popc(mlo);
-        const uint32_t a0 = cur + __popc(mlo & le) - 1, a1 = cur + nlo + __popc(mhi & le) - 1;
-        MIHG_DASSERT(a0 < n_ne && a1 < n_ne && s_off[wib][a0] <= t0 + lane && s_off[wib][a1] <= t0 + 32 + lane);
-        uint32_t e[2];
-        bool v[2];
-        v[0] = t0 + lane < total;
-        v[1] = t0 + 32 + lane < total;
-        e[0] = s_lo[wib][a0] + (t0 + lane - s_off[wib][a0]);
-        e[1] = s_lo[wib][a1] + (t0 + 32 + lane - s_off[wib][a1]);
-        cur += nlo + __popc(mhi);
-        verify_entries<W, kTrace>(p, ctx, v[0], e[0], v[1], e[1], qc, nw, n_new);
-      }
-      __syncwarp();
-    }
-    if (kTrace) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        n_cand += __shfl_xor_sync(~0u, n_cand, o);
-        n_new += __shfl_xor_sync(~0u, n_new, o);
-      }
-      if (lane == 0 && n_cand) {
-        atomicAdd(p.trc + 2 * uint64_t(q), (unsigned long long)n_cand);
-        if (n_new) atomicAdd(p.trc + 2 * uint64_t(q) + 1, (unsigned long long)n_new);
-      }
+      __threadfence();
+      __syncthreads();
+      if (s_done) break;
     }
   }
 }
@@ -936,6 +1034,28 @@ void dispatch_probe(const ProbeArgs& p, bool trace, cudaStream_t st) {
   }
 }
 
+// Per-query blocks for small batches (mih_solo_kernel; MIHG_SOLO=0 disables, MIHG_SOLO_BUDGET =
+// expected lookups of the whole batch below which it is used).
+template <int W>
+void launch_solo(const ProbeArgs& p, bool trace, uint32_t nq, uint32_t k, uint32_t bits, uint32_t* ubound,
+                 uint32_t* final_r, cudaStream_t st) {
+  const unsigned grid = unsigned(std::min<uint64_t>(nq, uint64_t(device_sm_count()) * probe_min_blocks(W, 2)));
+  if (trace) mih_solo_kernel<W, true, 2><<<grid, kProbeThreads, 0, st>>>(p, nq, k, bits, ubound, final_r);
+  else mih_solo_kernel<W, false, 2><<<grid, kProbeThreads, 0, st>>>(p, nq, k, bits, ubound, final_r);
+  MIHG_LAUNCH();
+}
+
+void dispatch_solo(const ProbeArgs& p, bool trace, uint32_t nq, uint32_t k, uint32_t bits, uint32_t* ubound,
+                   uint32_t* final_r, cudaStream_t st) {
+  switch (p.nw) {
+    case 1: launch_solo<1>(p, trace, nq, k, bits, ubound, final_r, st); break;
+    case 2: launch_solo<2>(p, trace, nq, k, bits, ubound, final_r, st); break;
+    case 3: launch_solo<3>(p, trace, nq, k, bits, ubound, final_r, st); break;
+    case 4: launch_solo<4>(p, trace, nq, k, bits, ubound, final_r, st); break;
+    default: launch_solo<0>(p, trace, nq, k, bits, ubound, final_r, st);
+  }
+}
+
 // Chunking of a round's (queries x ring) work list into warp units of 32 lanes x chunk probes.
 void plan_round(ProbeArgs& p, uint64_t nact) {
   p.lane_target = uint64_t(device_sm_count()) * 2048 * 4;  // lanes to keep busy
@@ -1142,6 +1262,7 @@ double uniform_model_lookups(const Index& idx, uint32_t k) {
 ProbeArgs make_probe_args(Index& idx, Workspace& ws, const uint64_t* d_q) {
   ProbeArgs p{};
   p.codes = idx.codes.get();
+  p.tables = idx.d_tables.get();
   p.n_codes = idx.n;
   p.qcodes = d_q;
   p.qsub = ws.qsub.get();
@@ -1327,6 +1448,36 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   // hopeless MIH: when the uniform model puts the lookups above 16x the scan budget, every query
   // goes to the exhaustive scan at round 0 (config 5, 256-bit uniform: ~220x; configs 1-4: < 1x)
   const bool pre_switch = alpha > 0 && uniform_model_lookups(idx, kstop) * probe_pairs >= 16.0 * alpha * scan_pairs;
+  // small batches of light queries: one block per query runs all its rounds (mih_solo_kernel)
+  const char* solo_env = std::getenv("MIHG_SOLO");  // read per call: tests run both paths
+  const bool solo_on = !(solo_env && solo_env[0] == '0');
+  const double solo_budget = std::getenv("MIHG_SOLO_BUDGET") ? std::atof(std::getenv("MIHG_SOLO_BUDGET")) : 4.0e6;
+  bool solo = solo_on && !part && !pre_switch && nq <= 65536 &&
+              double(nq) * uniform_model_lookups(idx, kstop) <= solo_budget;
+  for (uint32_t j = 0; solo && j < m; ++j) {  // no piece queue in there: buckets must fit the inline limit
+    const TableStorage& t = *idx.tables[j];
+    solo = t.max_bucket <= (t.dense ? p.inline_max : p.inline_max_sparse);
+  }
+  if (solo) {
+    for (uint32_t rr2 = 0; rr2 <= idx.bits; ++rr2) {
+      const uint32_t s2 = idx.lengths[rr2 % m];
+      acc += rr2 / m <= s2 ? host_binom(s2, rr2 / m) : 0;
+      lookups_prefix.push_back(acc);
+    }
+    ProbeArgs sp = p;
+    sp.d_nact = nullptr;
+    sp.pieces = nullptr;
+    sp.slice_bits = 0;
+    sp.part_bits = 0;
+    sp.rlimit = nullptr;
+    if (profst.enabled) MIHG_CUDA(cudaEventRecord(ws.ev_probe[0], st));
+    dispatch_solo(sp, d_tr != nullptr, uint32_t(nq), kstop, idx.bits, ws.ubound.get(), ws.final_r.get(), st);
+    if (profst.enabled) {
+      MIHG_CUDA(cudaEventRecord(ws.ev_probe[1], st));
+      probed_rounds.push_back(0);
+    }
+    nact_known = 0;
+  }
   uint32_t r = 0;
   for (; nact_known > 0; ++r) {
     if (r > idx.bits) throw CudaError("knn: radius loop exceeded the code width (internal error)");

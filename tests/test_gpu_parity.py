@@ -6,6 +6,21 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["rounds", "solo"])
+def search_path(request):
+    """Every case runs through both kNN drivers: the round-synchronous kernels (MIHG_SOLO=0) and,
+    where the batch is small enough to qualify, the one-block-per-query kernel (mih_solo_kernel)."""
+    import os
+
+    old = os.environ.get("MIHG_SOLO")
+    os.environ["MIHG_SOLO"] = "0" if request.param == "rounds" else "1"
+    yield request.param
+    if old is None:
+        os.environ.pop("MIHG_SOLO", None)
+    else:
+        os.environ["MIHG_SOLO"] = old
+
+
 def _mg():
     import paper_1307_2982_b200 as mg
 

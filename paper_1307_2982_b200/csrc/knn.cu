@@ -1455,7 +1455,7 @@ void knn_chunk(Index& idx, const uint64_t* d_q, uint64_t nq, uint32_t k, uint32_
   // (measured: a block per query loses to the round kernels once a query needs thousands of
   // lookups — config 2 / 3 / 4 at 100 queries: 0.6x / 0.45x / 0.1x — and ties at config 1 x 10000)
   const double model_lookups = uniform_model_lookups(idx, kstop);
-  bool solo = solo_on && !part && !pre_switch && nq <= 65536 && model_lookups <= 2048.0 &&
+  bool solo = solo_on && !part && !pre_switch && nq <= 65536 && model_lookups <= 4096.0 &&
               double(nq) * model_lookups <= solo_budget;
   for (uint32_t j = 0; solo && j < m; ++j) {  // no piece queue in there: buckets must fit the inline limit
     const TableStorage& t = *idx.tables[j];

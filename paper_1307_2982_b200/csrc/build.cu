@@ -218,14 +218,26 @@ __global__ void dir_build_kernel(const uint32_t* __restrict__ keys, uint64_t n, 
   __shared__ uint32_t cnt[8][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
-  for (uint64_t g = blockIdx.x * uint64_t(blockDim.x >> 5) + wib; g < ngroups; g += warps) {
+  // A warp takes 32 consecutive groups at a time: the 33 group boundaries are 32 + 1 binary
+  // searches run by the lanes in parallel (one dependent-load chain per 32 groups instead of one
+  // per group: the searches were the kernel's whole length), then the groups are built one by one.
+  for (uint64_t g0 = (blockIdx.x * uint64_t(blockDim.x >> 5) + wib) * 32; g0 < ngroups; g0 += warps * 32) {
+    if (kPhase == 1 && !__any_sync(~0u, g0 + lane < ngroups && flags[g0 + lane])) continue;
+    uint64_t lbv = lower_bound_u32(keys, n, (g0 + lane) << kDirBucketsLog2);
+    uint64_t ubv = __shfl_down_sync(~0u, lbv, 1);
+    {
+      uint64_t endv = 0;
+      if (lane == 0) endv = lower_bound_u32(keys, n, (g0 + 32) << kDirBucketsLog2);
+      endv = __shfl_sync(~0u, endv, 0);
+      if (lane == 31) ubv = endv;
+    }
+  for (uint32_t j = 0; j < 32; ++j) {
+    const uint64_t g = g0 + j;
+    if (g >= ngroups) break;
+    const uint64_t lb = __shfl_sync(~0u, lbv, j), ub = __shfl_sync(~0u, ubv, j);
     if (kPhase == 1 && !flags[g]) continue;
+    __syncwarp();
     cnt[wib][lane] = 0;
-    uint64_t lb = 0, ub = 0;
-    if (lane == 0) lb = lower_bound_u32(keys, n, g << kDirBucketsLog2);
-    if (lane == 1) ub = lower_bound_u32(keys, n, (g + 1) << kDirBucketsLog2);
-    lb = __shfl_sync(0xffffffffu, lb, 0);
-    ub = __shfl_sync(0xffffffffu, ub, 1);
     __syncwarp();
     for (uint64_t p = lb + lane; p < ub; p += 32) atomicAdd(&cnt[wib][keys[p] & 31u], 1u);
     __syncwarp();
@@ -266,6 +278,7 @@ __global__ void dir_build_kernel(const uint32_t* __restrict__ keys, uint64_t n, 
         dir[g].base = e;
       }
     }
+  }
   }
 }
 

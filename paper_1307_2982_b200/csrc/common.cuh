@@ -222,7 +222,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 inline uint32_t ceil_div_u32(uint64_t a, uint64_t b) { return uint32_t((a + b - 1) / b); }
 
 int device_sm_count();
-void configure_mempool(int device);  // keep freed stream-ordered memory cached (build.cu)
+void configure_mempool(int device);  // pool release threshold while an index is built (build.cu)
 void set_last_error(const std::string& msg);
 
 // Live per-kernel timing (CUDA events on the launching stream), enabled by mihg_profile_enable.

@@ -33,10 +33,19 @@ __global__ void __launch_bounds__(kSelThreads) select_small_kernel(SelectArgs a)
   // one pass: filtered keys go straight to shared memory while they fit; the count decides
   // afterwards whether the segment belongs to the large path (oversized: nothing was lost, the
   // large path re-reads the segment)
-  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const uint64_t key = a.keys[base + i];
-    if (keep_key(key, maxd)) {
-      const uint32_t at = atomicAdd(&s_cnt, 1u);
+  // (one shared-memory atomic per warp: every thread bumping the same counter serialised the
+  // whole block — the kernel's length at config 4)
+  const uint32_t lane = threadIdx.x & 31, ltm = (1u << lane) - 1u;
+  for (uint32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
+    const uint32_t i = i0 + threadIdx.x;
+    const uint64_t key = i < cnt ? a.keys[base + i] : ~0ull;
+    const bool keep = i < cnt && keep_key(key, maxd);
+    const uint32_t bal = __ballot_sync(~0u, keep);
+    uint32_t wbase = 0;
+    if (lane == 0 && bal) wbase = atomicAdd(&s_cnt, uint32_t(__popc(bal)));
+    wbase = __shfl_sync(~0u, wbase, 0);
+    if (keep) {
+      const uint32_t at = wbase + __popc(bal & ltm);
       if (at < kSmemKeys) sk[at] = key;
     }
   }
@@ -97,8 +106,14 @@ __global__ void __launch_bounds__(kSelThreads) select_small_kernel(SelectArgs a)
     }
     __syncthreads();
 #pragma unroll
-    for (uint32_t j = 0; j < kSmemKeys / kSelThreads; ++j)
-      if (mine[j] != ~0ull && uint32_t(mine[j] >> 32) <= D) sk[atomicAdd(&s_m, 1u)] = mine[j];
+    for (uint32_t j = 0; j < kSmemKeys / kSelThreads; ++j) {
+      const bool keep = mine[j] != ~0ull && uint32_t(mine[j] >> 32) <= D;
+      const uint32_t bal = __ballot_sync(~0u, keep);
+      uint32_t wbase = 0;
+      if (lane == 0 && bal) wbase = atomicAdd(&s_m, uint32_t(__popc(bal)));
+      wbase = __shfl_sync(~0u, wbase, 0);
+      if (keep) sk[wbase + __popc(bal & ltm)] = mine[j];
+    }
     __syncthreads();
     m = s_m;
   }

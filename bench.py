@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override database size (testing only)")
     ap.add_argument("--nq", type=int, default=0)
+    ap.add_argument("--single-layout", action="store_true",
+                    help="torchrun: skip the second multi-GPU layout's line (other_layout)")
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=0, help="queries per CPU-reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -716,6 +718,46 @@ def main():
         else:
             cpu = {"value": None, "unavailable": "oracle/_ref not built"}
 
+    # ---- N > 1 (torchrun): the OTHER multi-GPU layout beside the headline one, same workload,
+    # same timing rules, checked against the headline layout's answer (both are exact) ----
+    index_bytes = idx.device_bytes()
+    other_layout = None
+    if comm is not None and not args.single_layout:
+        pp2 = not probe_part
+        idx.close()
+        torch.cuda.empty_cache()
+        lo2, hi2 = (0, cfg["n"]) if pp2 else shard_range(cfg["n"], rank, world)
+        codes2 = make_codes_device(cfg, lo2, hi2, cfg["db_seed"], torch, dev, L)
+        idx = mg.MihIndex.build_from_device(codes2.data_ptr(), hi2 - lo2, bits, mg.consecutive_partition(bits, m),
+                                            local_rank, id_base=lo2)
+        del codes2
+        torch.cuda.empty_cache()
+        o_ids, o_d = torch.empty_like(out_ids), torch.empty_like(out_d)
+
+        def step2():
+            _lib.check(L.mihg_knn_sharded_device(idx._h, comm.handle, 0 if pp2 else 1, cfg["n"],
+                                                 C.c_void_p(queries.data_ptr()), nq, k, C.c_void_p(o_ids.data_ptr()),
+                                                 C.c_void_p(o_d.data_ptr()), None, C.c_void_p(stream.cuda_stream)))
+
+        for _ in range(max(args.warmup, 3)):
+            step2()
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step2()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        tt = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms2 = float(tt.item())
+        same = torch.tensor([1 if (torch.equal(o_ids, res_ids) and torch.equal(o_d, res_d)) else 0], device=dev)
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        other_layout = {"parallelism": ("probe-space partition x%d (replicated index)" if pp2
+                                        else "id-range shards x%d (north_star layout)") % world,
+                        "value": nq * args.steps / (ms2 / 1000.0), "unit": "queries/s",
+                        "ms_per_step": ms2 / args.steps, "same_answer_as_headline_layout": bool(same.item())}
+
     if rank == 0:
         line = {
             "metric": "exact kNN queries/s", "value": value, "unit": "queries/s", "n_gpus": world,
@@ -725,8 +767,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(nq * W * 8),
                     "d2h_bytes_per_step": int(nq * k * 8)},
             "gpu_launches": launches, "verified_vs_scan": verified, "parity": parity, "roofline": roofline,
-            "cpu_baseline": cpu, "clocks": clk,
-            "setup": {"gen_s": gen_s, "index_build_s": build_s, "index_device_bytes": idx.device_bytes()},
+            "cpu_baseline": cpu, "clocks": clk, "other_layout": other_layout,
+            "setup": {"gen_s": gen_s, "index_build_s": build_s, "index_device_bytes": index_bytes},
         }
         emit(line)
     idx.close()

@@ -12,6 +12,7 @@ KERNELS = [("tc_scan_kernelILi256ELb0ELb1E", "K7 tensor-core scan, 256-bit, CTA 
            ("mih_probe_kernelILi1ELb0ELi4E", "K4 MIH probe, 64-bit, untraced, 4 probes/lane (sparse tables)"),
            ("mih_probe_kernelILi1ELb0ELi2E", "K4 MIH probe, 64-bit, untraced, 2 probes/lane (dense tables)"),
            ("mih_piece_kernelILi1ELb0E", "K4b MIH big-bucket pieces, 64-bit"),
+           ("mih_solo_kernelILi1ELb0ELi2E", "K4s one block per query (light batches), 64-bit"),
            ("scan_kernel", "K6 POPC scan")]
 WATCH = ["UTCIMMA", "UTCBAR", "UTCATOMSWS", "LDTM", "STTM", "UBLKCP", "SYNCS", "ELECT", "UCGABAR", "STL", "LDL",
          "POPC", "LDG", "STG", "ATOMG", "ATOMS", "RED", "LDS", "STS", "VIMNMX", "IMNMX", "SHFL", "VOTE", "BAR", "MEMBAR"]
